@@ -1,0 +1,145 @@
+/*
+ * sto.h -- C ABI of the B200-native coupled spin-torque-oscillator simulator.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (`spinosc`, pure Python) has no FFI of its own; these entry points are what
+ * its plugin layer binds (see INTEGRATION.md for the ctypes stub a spinosc
+ * maintainer registers via `spinosc.backends.register_backend`):
+ *
+ *   sto_probe            <- backends/gpu.py:34-37        is_available()
+ *   sto_plan_create      <- backends/gpu.py:55-77        TorchBackend.__init__ (W, W_in
+ *                                                         resident on the device once)
+ *   sto_derivative       <- backends/__init__.py:5-7,48-50  derivative(m, u, out) contract
+ *                           (model.py:206-302 llg_derivative; gpu.py:83-119)
+ *   sto_integrate        <- integrator.py:131-187 integrate() time loop with
+ *                           integrator.py:91-121 rk4_step, fused into one
+ *                           persistent kernel (no per-step launch)
+ *   sto_tree_matvec      <- model.py:55-63 tree_matvec (pinned adjacent-pairs tree)
+ *   status codes         <- errors.py (ParameterError, BackendUnavailableError,
+ *                           IntegrationDivergedError(oscillator, step))
+ *
+ * Conventions: plain pointers and sizes only.  Pointers documented "device"
+ * must be device (or managed) memory of the plan's device; "any" accepts host
+ * or device memory (UVA, cudaMemcpyDefault).  `stream` is a cudaStream_t
+ * passed as void* (NULL = legacy default stream).  All state arrays are
+ * row-major (n, 3) float64, exactly the numpy layout of the reference.
+ * Every function returns STO_OK or an error code; sto_last_error() gives a
+ * thread-local message for the last failure.  A plan is not thread-safe.
+ */
+#ifndef STO_H
+#define STO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STO_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define STO_API __attribute__((visibility("default")))
+#else
+#define STO_API
+#endif
+
+enum sto_status_code {
+    STO_OK = 0,
+    STO_E_UNAVAILABLE = 1, /* no usable sm_100 device    -> BackendUnavailableError */
+    STO_E_PARAM = 2,       /* bad sizes / pointers       -> ParameterError          */
+    STO_E_DIVERGED = 3,    /* non-finite recorded state  -> IntegrationDivergedError */
+    STO_E_CUDA = 4,        /* CUDA runtime failure       -> SpinoscError             */
+    STO_E_NOMEM = 5        /* device allocation failed   -> SpinoscError             */
+};
+
+/* The 11 right-hand-side scalars, in the order of the reference's
+ * `_scalar_pack` (backends/cpu_jit.py:118-122). */
+enum sto_const_index {
+    STO_C_PREC = 0, STO_C_DAMP, STO_H_APPL, STO_H_ANISO, STO_H_S_PREFACTOR,
+    STO_LAMBDA, STO_A_CP, STO_A_IN, STO_PX, STO_PY, STO_PZ, STO_N_CONSTS
+};
+
+typedef struct sto_plan sto_plan;
+
+typedef struct {
+    int64_t n;            /* oscillators (rows and columns of W)                 */
+    int64_t n_in;         /* input channels (columns of W_in)                    */
+    const double *w_cp;   /* any: (n, ld_cp) row-major coupling W                */
+    int64_t ld_cp;        /* row stride of w_cp in elements (>= n)               */
+    const double *w_in;   /* any: (n, ld_in) row-major input weights             */
+    int64_t ld_in;        /* row stride of w_in in elements (>= n_in)            */
+    double consts[STO_N_CONSTS];
+    int device;           /* CUDA device ordinal                                 */
+    int flags;            /* STO_PLAN_* bits                                     */
+} sto_plan_desc;
+
+/* Force a kernel family (testing / benchmarking); default = automatic. */
+#define STO_PLAN_FORCE_STREAM   0x1  /* W streamed from HBM/L2 every stage        */
+#define STO_PLAN_FORCE_RESIDENT 0x2  /* W slice held in shared memory per CTA     */
+#define STO_PLAN_FORCE_SINGLE   0x4  /* one CTA, exchange through shared memory   */
+#define STO_PLAN_NO_TINY        0x8  /* do not use the one-warp kernel for n<=32  */
+
+typedef struct {
+    double *m;               /* device (n,3): initial state in, final state out    */
+    const double *samples;   /* device (n_samples, n_in) zero-order-hold drive      */
+    int64_t n_samples;
+    int64_t steps_per_sample;
+    double dt;               /* h2 = dt*0.5 and dt/6.0 are formed inside, in IEEE   */
+    int64_t steps;
+    int64_t record_stride;   /* grid {0, s, 2s, ...} u {steps} (integrator.py:124)  */
+    double *states;          /* device (n_records, n, 3); states[0] = m0 is written */
+} sto_run;
+
+typedef struct {
+    int32_t diverged;        /* 1 when a recorded state was non-finite              */
+    int32_t reserved;
+    int64_t oscillator;      /* first row with a non-finite component               */
+    int64_t step;            /* recorded step at which it was seen                  */
+} sto_status;
+
+typedef struct {
+    int32_t kernel;          /* 0 tiny, 1 single-CTA, 2 SMEM-resident grid, 3 streaming grid */
+    int32_t grid;            /* CTAs of the persistent kernel                        */
+    int32_t threads;         /* threads per CTA                                      */
+    int32_t smem_bytes;      /* dynamic shared memory per CTA                        */
+    int64_t ldw;             /* padded row width of the device W layout              */
+    int64_t block_cols;      /* columns per (row, block) work unit                   */
+    int64_t w_bytes;         /* device bytes of the W layout                          */
+} sto_plan_info;
+
+STO_API const char *sto_last_error(void);
+STO_API int sto_abi_version(void);
+
+/* 1 if `device` is an sm_100-class GPU this library can drive, else 0. */
+STO_API int sto_probe(int device);
+STO_API int64_t sto_n_records(int64_t steps, int64_t record_stride);
+
+STO_API int sto_plan_create(sto_plan **plan, const sto_plan_desc *desc);
+STO_API void sto_plan_destroy(sto_plan *plan);
+STO_API int sto_plan_get_info(const sto_plan *plan, sto_plan_info *info);
+
+/* out = dm/dt at state m under drive u.  m, u, out: device. Asynchronous. */
+STO_API int sto_derivative(sto_plan *plan, const double *m, const double *u, double *out,
+                   void *stream);
+
+/* Whole RK4 run in one persistent launch.  If `status` is non-NULL the call
+ * synchronises the stream, fills it and returns STO_E_DIVERGED on divergence;
+ * with NULL it is asynchronous and sto_plan_last_status() reads it later. */
+STO_API int sto_integrate(sto_plan *plan, const sto_run *run, sto_status *status, void *stream);
+STO_API int sto_plan_last_status(sto_plan *plan, sto_status *status, void *stream);
+
+/* Host-buffer variant (the e2e path): m, samples, states are HOST pointers;
+ * copies in and out are done inside (pinned staging), then synchronises. */
+STO_API int sto_integrate_host(sto_plan *plan, double *m, const double *samples, int64_t n_samples,
+                       int64_t steps_per_sample, double dt, int64_t steps,
+                       int64_t record_stride, double *states, sto_status *status);
+
+/* out[r] = pinned-tree sum_j a[r, j] * x[j] (model.py:55-63).
+ * a: any (rows, lda); x: any (cols); out: any (rows).  Synchronous. */
+STO_API int sto_tree_matvec(int device, int64_t rows, int64_t cols, const double *a, int64_t lda,
+                    const double *x, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STO_H */

@@ -1,0 +1,216 @@
+"""ctypes binding of libsto_b200.so (the C ABI in include/sto.h).
+
+There is no fallback: if the library is missing or no sm_100 device is
+present, every entry point raises (`BackendUnavailableError` for the probe
+path, `SpinoscError` otherwise). Device buffers are torch tensors; only raw
+pointers and sizes cross the ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+from .errors import (BackendUnavailableError, IntegrationDivergedError, ParameterError,
+                     SpinoscError)
+
+LIB_PATH = Path(__file__).resolve().parent / "libsto_b200.so"
+
+STO_OK, STO_E_UNAVAILABLE, STO_E_PARAM, STO_E_DIVERGED, STO_E_CUDA, STO_E_NOMEM = range(6)
+
+# flags of sto_plan_desc (include/sto.h)
+FORCE_STREAM, FORCE_RESIDENT, FORCE_SINGLE, NO_TINY = 0x1, 0x2, 0x4, 0x8
+KERNEL_NAMES = {0: "tiny", 1: "single", 2: "resident", 3: "stream"}
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("n_in", ctypes.c_int64),
+                ("w_cp", ctypes.c_void_p), ("ld_cp", ctypes.c_int64),
+                ("w_in", ctypes.c_void_p), ("ld_in", ctypes.c_int64),
+                ("consts", ctypes.c_double * 11), ("device", ctypes.c_int),
+                ("flags", ctypes.c_int)]
+
+
+class Run(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_void_p), ("samples", ctypes.c_void_p),
+                ("n_samples", ctypes.c_int64), ("steps_per_sample", ctypes.c_int64),
+                ("dt", ctypes.c_double), ("steps", ctypes.c_int64),
+                ("record_stride", ctypes.c_int64), ("states", ctypes.c_void_p)]
+
+
+class Status(ctypes.Structure):
+    _fields_ = [("diverged", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("oscillator", ctypes.c_int64), ("step", ctypes.c_int64)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int32), ("grid", ctypes.c_int32),
+                ("threads", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
+                ("ldw", ctypes.c_int64), ("block_cols", ctypes.c_int64),
+                ("w_bytes", ctypes.c_int64)]
+
+
+# every symbol include/sto.h declares, with its ctypes signature
+SIGNATURES = {
+    "sto_last_error": (ctypes.c_char_p, []),
+    "sto_abi_version": (ctypes.c_int, []),
+    "sto_probe": (ctypes.c_int, [ctypes.c_int]),
+    "sto_n_records": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int64]),
+    "sto_plan_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(PlanDesc)]),
+    "sto_plan_destroy": (None, [ctypes.c_void_p]),
+    "sto_plan_get_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PlanInfo)]),
+    "sto_derivative": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p]),
+    "sto_integrate": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Run),
+                                     ctypes.POINTER(Status), ctypes.c_void_p]),
+    "sto_plan_last_status": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Status),
+                                            ctypes.c_void_p]),
+    "sto_integrate_host": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p,
+                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                          ctypes.c_int64, ctypes.c_int64, _c_double_p,
+                                          ctypes.POINTER(Status)]),
+    "sto_tree_matvec": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                       _c_double_p, ctypes.c_int64, _c_double_p, _c_double_p]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libsto_b200.so once; raise loudly when it is absent."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise SpinoscError(
+                f"{LIB_PATH.name} is not built; run `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` (or `make -C paper_2312_01121_b200/csrc`)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().sto_last_error().decode(errors="replace")
+
+
+def check(rc: int, status: Status | None = None) -> None:
+    if rc == STO_OK:
+        return
+    msg = last_error()
+    if rc == STO_E_DIVERGED and status is not None:
+        raise IntegrationDivergedError(oscillator=status.oscillator, step=status.step)
+    if rc == STO_E_PARAM:
+        raise ParameterError(msg)
+    if rc == STO_E_UNAVAILABLE:
+        raise BackendUnavailableError("gpu", [])
+    raise SpinoscError(f"sto error {rc}: {msg}")
+
+
+def probe(device: int = 0) -> bool:
+    """True when the library loads and `device` is an sm_100 GPU (never raises)."""
+    try:
+        return bool(lib().sto_probe(int(device)))
+    except Exception:
+        return False
+
+
+def n_records(steps: int, stride: int) -> int:
+    return int(lib().sto_n_records(steps, stride))
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_ptr(device: int):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class Plan:
+    """Owns a device-resident W layout + launch configuration (sto_plan)."""
+
+    def __init__(self, w_cp: np.ndarray, w_in: np.ndarray, consts, device: int = 0,
+                 flags: int = 0):
+        w_cp = np.ascontiguousarray(w_cp, dtype=np.float64)
+        w_in = np.ascontiguousarray(w_in, dtype=np.float64)
+        if w_cp.ndim != 2 or w_cp.shape[0] != w_cp.shape[1]:
+            raise ParameterError("coupling matrix must be square")
+        if w_in.ndim != 2 or w_in.shape[0] != w_cp.shape[0]:
+            raise ParameterError("input weights must be (n, n_in)")
+        self.n, self.n_in = w_cp.shape[0], w_in.shape[1]
+        self.device = int(device)
+        d = PlanDesc(n=self.n, n_in=self.n_in, w_cp=w_cp.ctypes.data, ld_cp=self.n,
+                     w_in=w_in.ctypes.data, ld_in=self.n_in, device=self.device, flags=flags)
+        for i, v in enumerate(consts):
+            d.consts[i] = float(v)
+        h = ctypes.c_void_p()
+        check(lib().sto_plan_create(ctypes.byref(h), ctypes.byref(d)))
+        self._h = h
+        info = PlanInfo()
+        check(lib().sto_plan_get_info(self._h, ctypes.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in PlanInfo._fields_}
+        self.info["kernel_name"] = KERNEL_NAMES.get(info.kernel, "?")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().sto_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- device-pointer entry points (torch CUDA tensors) -----------------
+    def derivative_dev(self, m, u, out) -> None:
+        check(lib().sto_derivative(self._h, m.data_ptr(), u.data_ptr(), out.data_ptr(),
+                                   _stream_ptr(self.device)))
+
+    def integrate_dev(self, m, samples, steps_per_sample: int, dt: float, steps: int,
+                      stride: int, states, sync: bool = True) -> Status:
+        run = Run(m=m.data_ptr(), samples=samples.data_ptr(), n_samples=samples.shape[0],
+                  steps_per_sample=int(steps_per_sample), dt=float(dt), steps=int(steps),
+                  record_stride=int(stride),
+                  states=states.data_ptr() if states is not None else None)
+        st = Status()
+        rc = lib().sto_integrate(self._h, ctypes.byref(run),
+                                 ctypes.byref(st) if sync else None, _stream_ptr(self.device))
+        check(rc, st)
+        return st
+
+    def last_status(self) -> Status:
+        st = Status()
+        check(lib().sto_plan_last_status(self._h, ctypes.byref(st), _stream_ptr(self.device)),
+              st)
+        return st
+
+
+def tree_matvec(matrix, vec, out=None, device: int | None = None):
+    """Pinned-tree (matrix @ vec) on the GPU (model.py:55-63 semantics)."""
+    a = np.ascontiguousarray(np.asarray(matrix, dtype=np.float64))
+    x = np.ascontiguousarray(np.asarray(vec, dtype=np.float64))
+    if a.ndim != 2 or x.ndim != 1 or a.shape[1] != x.shape[0]:
+        raise ParameterError("tree_matvec needs a (rows, cols) matrix and a (cols,) vector")
+    res = np.empty(a.shape[0])
+    if device is None:
+        device = int(os.environ.get("SPINOSC_GPU_DEVICE", 0))
+    check(lib().sto_tree_matvec(int(device), a.shape[0], a.shape[1],
+                                a.ctypes.data_as(_c_double_p), a.shape[1],
+                                x.ctypes.data_as(_c_double_p), res.ctypes.data_as(_c_double_p)))
+    if out is None:
+        return res
+    np.copyto(out, res)
+    return out

@@ -1,0 +1,133 @@
+"""The registered "gpu" backend: B200 persistent-kernel RK4 (sm_100a).
+
+Replaces the reference's `TorchBackend` (`backends/gpu.py:49-119`) behind
+the same registry id and factory signature. Two entry points:
+
+* `derivative(m, u, out)` -- the reference plugin contract
+  (`backends/__init__.py:5-7, 48-50`), one fused K0 launch. numpy arrays
+  pay an H2D/D2H per call exactly like `gpu.py:87-88,118`; CUDA torch
+  tensors are used in place (no copies), which is what
+  `time_derivative_eval` wants to time.
+* `integrate_run(m0, series, dt, steps, stride)` -- the whole time loop in
+  one persistent launch; `integrate()` prefers it whenever present.
+
+Device selection follows `gpu.py:40-46`: explicit argument, then the
+SPINOSC_GPU_DEVICE environment variable, then 0; "cuda:<i>" strings are
+accepted. Any non-CUDA device raises `BackendUnavailableError`: there is no
+CPU evaluation behind this backend.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+from .. import _native
+from ..errors import BackendUnavailableError, ParameterError
+from ..params import kernel_scalars
+
+ENV_DEVICE = "SPINOSC_GPU_DEVICE"
+
+
+def is_available(device=None) -> bool:
+    try:
+        return _native.probe(resolve_device(device))
+    except BackendUnavailableError:
+        return False
+
+
+def resolve_device(device=None) -> int:
+    """Device ordinal from argument / env var / default 0 (ref `gpu.py:40-46`)."""
+    if device is None:
+        device = os.environ.get(ENV_DEVICE, 0)
+    if isinstance(device, str) and device.startswith("cuda"):
+        device = device.split(":", 1)[1] if ":" in device else 0
+    try:
+        return int(device)
+    except (TypeError, ValueError):
+        from . import available_backend_ids
+
+        raise BackendUnavailableError("gpu", available_backend_ids()) from None
+
+
+class B200Backend:
+    """Coupled-STO equation of motion and RK4 time loop on one B200."""
+
+    backend_id = "gpu"
+    kind = "B200 persistent RK4 (sm_100a)"
+
+    def __init__(self, topology, params, device=None, flags: int = 0, consts=None):
+        """`consts` overrides the 11 kernel scalars derived from `params`;
+        `flags` forces a kernel family (_native.FORCE_*; testing/benchmarks)."""
+        self.device_index = resolve_device(device)
+        if not _native.probe(self.device_index):
+            from . import available_backend_ids
+
+            raise BackendUnavailableError("gpu", available_backend_ids())
+        import torch
+
+        self._torch = torch
+        self._dev = torch.device("cuda", self.device_index)
+        self.n, self.n_in = topology.n, topology.n_in
+        self._plan = _native.Plan(topology.coupling.entries, topology.input_weights.entries,
+                                  kernel_scalars(params) if consts is None else consts,
+                                  device=self.device_index, flags=flags)
+        self.last_kernel_seconds = float("nan")
+
+    @property
+    def device(self) -> str:
+        return str(self._dev)
+
+    @property
+    def plan_info(self) -> dict:
+        return dict(self._plan.info)
+
+    def close(self) -> None:
+        self._plan.close()
+
+    # ------------------------------------------------------------------
+    def derivative(self, m, u, out):
+        """Write dm/dt at (m, u) into `out` (numpy or CUDA torch tensors)."""
+        t = self._torch
+        if isinstance(m, t.Tensor) and m.is_cuda:
+            self._plan.derivative_dev(m, u, out)
+            return out
+        m_d = t.as_tensor(np.ascontiguousarray(m, dtype=np.float64)).to(self._dev)
+        u_d = t.as_tensor(np.ascontiguousarray(u, dtype=np.float64)).to(self._dev)
+        if m_d.shape != (self.n, 3) or u_d.shape != (self.n_in,):
+            raise ParameterError("derivative expects m (n, 3) and u (n_in,)")
+        out_d = t.empty_like(m_d)
+        self._plan.derivative_dev(m_d, u_d, out_d)
+        np.copyto(out, out_d.cpu().numpy())
+        return out
+
+    def integrate_run(self, m0: np.ndarray, samples: np.ndarray, steps_per_sample: int,
+                      dt: float, steps: int, stride: int) -> np.ndarray:
+        """Run the whole RK4 loop on the device; returns the recorded states.
+
+        m0 is updated in place to the final state. Raises
+        IntegrationDivergedError(oscillator, step) like `integrator.py:174-177`.
+        """
+        t = self._torch
+        nrec = _native.n_records(steps, stride)
+        with t.cuda.device(self._dev):
+            m_d = t.as_tensor(np.ascontiguousarray(m0, dtype=np.float64)).to(self._dev)
+            s_d = t.as_tensor(np.ascontiguousarray(samples, dtype=np.float64)).to(self._dev)
+            states_d = t.empty((nrec, self.n, 3), dtype=t.float64, device=self._dev)
+            start, stop = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+            start.record()
+            self._plan.integrate_dev(m_d, s_d, steps_per_sample, dt, steps, stride, states_d,
+                                     sync=False)
+            stop.record()
+            stop.synchronize()
+            self.last_kernel_seconds = start.elapsed_time(stop) / 1e3
+            self._plan.last_status()  # raises IntegrationDivergedError on divergence
+            states = states_d.cpu().numpy()
+            np.copyto(m0, m_d.cpu().numpy())
+        return states
+
+
+def make_backend(topology, params, workers=None, gpu_device=None):
+    """Registry factory, signature of ref `backends/__init__.py:48-50`."""
+    return B200Backend(topology, params, device=gpu_device)

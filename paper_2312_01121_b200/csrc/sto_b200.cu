@@ -1,0 +1,502 @@
+// sto_b200.cu -- C-ABI implementation (include/sto.h) of the B200-native
+// coupled spin-torque-oscillator RK4 path.  Build: see csrc/Makefile
+// (nvcc -gencode arch=compute_100a,code=sm_100a -fmad=false -lineinfo).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/sto.h"
+#include "sto_kernels.cuh"
+
+using namespace sto;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define STO_CUDA(call)                                                                       \
+    do {                                                                                     \
+        cudaError_t _e = (call);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            return fail(_e == cudaErrorMemoryAllocation ? STO_E_NOMEM : STO_E_CUDA,          \
+                        std::string(#call) + ": " + cudaGetErrorString(_e));                 \
+    } while (0)
+
+constexpr int kThreads = 512;
+constexpr size_t kSmemBudget = 220 * 1024;  // of 227 KB opt-in per CTA
+
+// Column schedule for `n` logical columns (see sto_device.cuh).
+ColSched make_sched(int n, int blk_hint) {
+    ColSched s{};
+    s.n = n;
+    s.nfull = n / kSegFull;
+    int rem = n - s.nfull * kSegFull;
+    int pos = s.nfull * kSegFull;
+    const int sizes[3] = {256, 128, 64};
+    for (int i = 0; i < 3; ++i) {
+        if (rem >= sizes[i]) {
+            s.tail_base[s.ntail] = pos;
+            s.tail_c[s.ntail] = sizes[i] / 32;
+            ++s.ntail;
+            pos += sizes[i];
+            rem -= sizes[i];
+        }
+    }
+    if (rem > 0) {
+        s.tail_base[s.ntail] = pos;
+        s.tail_c[s.ntail] = 2;
+        ++s.ntail;
+        pos += 64;
+    }
+    s.ldw = pos;
+    int blk = kSegFull;
+    while (blk < blk_hint && blk < kSegFull * kMaxLeaves) blk <<= 1;
+    s.blk = blk;
+    s.nblocks = (s.ldw + blk - 1) / blk;
+    return s;
+}
+
+// physical -> logical column (inverse of col_perm); -1 for padding
+__host__ __device__ inline int col_unperm(const ColSched &s, int p) {
+    int base, c;
+    if (p < s.nfull * kSegFull) {
+        base = p & ~(kSegFull - 1);
+        c = 16;
+    } else {
+        base = -1;
+        c = 2;
+        for (int t = 0; t < s.ntail; ++t)
+            if (p >= s.tail_base[t] && p < s.tail_base[t] + 32 * s.tail_c[t]) {
+                base = s.tail_base[t];
+                c = s.tail_c[t];
+            }
+        if (base < 0) return -1;
+    }
+    const int o = p - base;
+    const int vec = o >> 1, half = o & 1;
+    const int l = vec & 31, i = vec >> 5;
+    const int k = base + l * c + 2 * i + half;
+    return k < s.n ? k : -1;
+}
+
+__global__ void permute_rows_kernel(const double *__restrict__ src, long long lds,
+                                    double *__restrict__ dst, int rows, ColSched cs) {
+    const long long total = (long long)rows * cs.ldw;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / cs.ldw);
+        const int pcol = (int)(i - (long long)r * cs.ldw);
+        const int k = col_unperm(cs, pcol);
+        dst[i] = k >= 0 ? src[(long long)r * lds + k] : -0.0;  // -0.0: exact identity
+    }
+}
+
+__global__ void reset_status_kernel(StatusDev *st, unsigned long long *bar) {
+    st->flag = 0;
+    st->oscillator = 0x7fffffffffffffffLL;
+    st->step = -1;
+    *bar = 0ull;
+}
+
+struct Layout {
+    ColSched cs{};
+    int rows = 0;
+    double *w = nullptr;
+};
+
+int upload_layout(Layout &L, int rows, int cols, const double *a, long long lda, int blk_hint,
+                  cudaStream_t stream) {
+    L.rows = rows;
+    L.cs = make_sched(cols, blk_hint);
+    const size_t bytes = (size_t)rows * L.cs.ldw * sizeof(double);
+    STO_CUDA(cudaMalloc(&L.w, bytes));
+    double *stage = nullptr;
+    STO_CUDA(cudaMalloc(&stage, (size_t)rows * cols * sizeof(double)));
+    STO_CUDA(cudaMemcpy2DAsync(stage, (size_t)cols * sizeof(double), a, (size_t)lda * sizeof(double),
+                               (size_t)cols * sizeof(double), rows, cudaMemcpyDefault, stream));
+    permute_rows_kernel<<<1184, 256, 0, stream>>>(stage, cols, L.w, rows, L.cs);
+    STO_CUDA(cudaGetLastError());
+    STO_CUDA(cudaStreamSynchronize(stream));
+    STO_CUDA(cudaFree(stage));
+    return STO_OK;
+}
+
+enum KernelKind { kTiny = 0, kSingle = 1, kResident = 2, kStream = 3 };
+
+}  // namespace
+
+struct sto_plan {
+    int device = 0;
+    int sm_count = 0;
+    long long l2_bytes = 0;
+    int n = 0, n_in = 0;
+    Consts c{};
+    Layout L;
+    double *w_in = nullptr;
+    double *xbuf = nullptr;
+    unsigned long long *bar = nullptr;
+    StatusDev *status = nullptr;
+    // integrate launch configuration
+    int kind = kStream;
+    bool stream_evict_first = true;
+    int grid = 1;
+    int rows_cap = 1;
+    int chunk_cols = 0;
+    size_t smem = 0;
+};
+
+namespace {
+
+size_t grid_smem(int rows_cap, const ColSched &cs, int chunk_cols, bool resident) {
+    size_t d = (size_t)chunk_cols + (resident ? (size_t)rows_cap * cs.ldw : 0) +
+               (size_t)rows_cap * cs.nblocks + 13 * (size_t)rows_cap + 2;
+    return d * sizeof(double);
+}
+
+int choose_chunk(const ColSched &cs, int rows_cap, bool resident) {
+    if (grid_smem(rows_cap, cs, cs.ldw, resident) <= kSmemBudget) return cs.ldw;
+    int chunk = 16384;
+    while (chunk > cs.blk && grid_smem(rows_cap, cs, chunk, resident) > kSmemBudget) chunk >>= 1;
+    return std::max(chunk, cs.blk);
+}
+
+template <WSrc S, bool SINGLE>
+int launch_grid(const KParams &p, int grid, size_t smem, bool cooperative, cudaStream_t stream) {
+    auto fn = grid_rk4_kernel<S, SINGLE>;
+    STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (cooperative) {
+        void *args[] = {(void *)&p};
+        STO_CUDA(cudaLaunchCooperativeKernel((void *)fn, dim3(grid), dim3(kThreads), args, smem,
+                                             stream));
+    } else {
+        fn<<<grid, kThreads, smem, stream>>>(p);
+        STO_CUDA(cudaGetLastError());
+    }
+    return STO_OK;
+}
+
+int launch_tiny(const KParams &p, int n, cudaStream_t stream) {
+    if (n <= 1) tiny_rk4_kernel<1><<<1, 32, 0, stream>>>(p);
+    else if (n <= 2) tiny_rk4_kernel<2><<<1, 32, 0, stream>>>(p);
+    else if (n <= 4) tiny_rk4_kernel<4><<<1, 32, 0, stream>>>(p);
+    else if (n <= 8) tiny_rk4_kernel<8><<<1, 32, 0, stream>>>(p);
+    else if (n <= 16) tiny_rk4_kernel<16><<<1, 32, 0, stream>>>(p);
+    else tiny_rk4_kernel<32><<<1, 32, 0, stream>>>(p);
+    STO_CUDA(cudaGetLastError());
+    return STO_OK;
+}
+
+KParams base_params(const sto_plan *P) {
+    KParams p{};
+    p.cs = P->L.cs;
+    p.c = P->c;
+    p.rows = P->n;
+    p.n_in = P->n_in;
+    p.w = P->L.w;
+    p.w_in = P->w_in;
+    p.xbuf = P->xbuf;
+    p.bar = P->bar;
+    p.status = P->status;
+    p.x_stride = 1;
+    p.n_samples = 1;
+    p.sps = 1;
+    p.steps = 1;
+    p.stride = 1;
+    return p;
+}
+
+int check_device(int device, cudaDeviceProp *prop) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count)
+        return fail(STO_E_UNAVAILABLE, "no CUDA device " + std::to_string(device));
+    STO_CUDA(cudaGetDeviceProperties(prop, device));
+    if (prop->major != 10)
+        return fail(STO_E_UNAVAILABLE, std::string("device is not sm_100-class: ") + prop->name);
+    return STO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sto_last_error(void) { return g_err.c_str(); }
+
+int sto_abi_version(void) { return STO_ABI_VERSION; }
+
+int sto_probe(int device) {
+    cudaDeviceProp prop;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) return 0;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return 0;
+    return prop.major == 10 ? 1 : 0;
+}
+
+int64_t sto_n_records(int64_t steps, int64_t record_stride) {
+    if (steps < 1 || record_stride < 1) return 0;
+    return steps / record_stride + 1 + (steps % record_stride != 0 ? 1 : 0);
+}
+
+int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
+    if (!out || !d) return fail(STO_E_PARAM, "null plan or descriptor");
+    *out = nullptr;
+    if (d->n < 1 || d->n_in < 1 || d->n > (1 << 24) || d->n_in > (1 << 20))
+        return fail(STO_E_PARAM, "n and n_in must be >= 1");
+    if (!d->w_cp || !d->w_in || d->ld_cp < d->n || d->ld_in < d->n_in)
+        return fail(STO_E_PARAM, "bad W / W_in pointers or leading dimensions");
+    cudaDeviceProp prop;
+    if (int rc = check_device(d->device, &prop)) return rc;
+    STO_CUDA(cudaSetDevice(d->device));
+
+    sto_plan *P = new sto_plan();
+    P->device = d->device;
+    P->sm_count = prop.multiProcessorCount;
+    P->l2_bytes = prop.l2CacheSize;
+    P->n = (int)d->n;
+    P->n_in = (int)d->n_in;
+    const double *k = d->consts;
+    P->c = Consts{k[0], k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8], k[9], k[10]};
+
+    auto bail = [&](int rc) {
+        sto_plan_destroy(P);
+        return rc;
+    };
+    cudaStream_t s = nullptr;
+    const int n = P->n;
+    const int blk_hint = n >= 8192 ? 2048 : 512;
+    if (int rc = upload_layout(P->L, n, n, d->w_cp, d->ld_cp, blk_hint, s)) return bail(rc);
+    const ColSched &cs = P->L.cs;
+    if (cudaMalloc(&P->w_in, sizeof(double) * (size_t)n * d->n_in) != cudaSuccess ||
+        cudaMalloc(&P->xbuf, sizeof(double) * 2 * (size_t)cs.ldw) != cudaSuccess ||
+        cudaMalloc(&P->bar, 64) != cudaSuccess ||
+        cudaMalloc(&P->status, sizeof(StatusDev)) != cudaSuccess)
+        return bail(fail(STO_E_NOMEM, "device allocation failed"));
+    if (cudaMemcpy2D(P->w_in, sizeof(double) * d->n_in, d->w_in, sizeof(double) * d->ld_in,
+                     sizeof(double) * d->n_in, n, cudaMemcpyDefault) != cudaSuccess ||
+        cudaMemset(P->xbuf, 0, sizeof(double) * 2 * (size_t)cs.ldw) != cudaSuccess)
+        return bail(fail(STO_E_CUDA, "W_in upload failed"));
+
+    // ---- choose the integrate kernel ------------------------------------
+    const bool no_tiny = d->flags & STO_PLAN_NO_TINY;
+    const size_t single_smem = grid_smem(n, cs, cs.ldw, true);
+    if (n <= 32 && !no_tiny && !(d->flags & (STO_PLAN_FORCE_STREAM | STO_PLAN_FORCE_RESIDENT |
+                                             STO_PLAN_FORCE_SINGLE))) {
+        P->kind = kTiny;
+        P->grid = 1;
+    } else if ((d->flags & STO_PLAN_FORCE_SINGLE) ||
+               (!(d->flags & (STO_PLAN_FORCE_STREAM | STO_PLAN_FORCE_RESIDENT)) && n <= 128 &&
+                single_smem <= kSmemBudget)) {
+        if (single_smem > kSmemBudget)
+            return bail(fail(STO_E_PARAM, "single-CTA kernel does not fit shared memory"));
+        P->kind = kSingle;
+        P->grid = 1;
+        P->rows_cap = n;
+        P->chunk_cols = cs.ldw;
+        P->smem = single_smem;
+    } else {
+        int g = std::min(P->sm_count, n);
+        P->rows_cap = (n + g - 1) / g;
+        const size_t res_smem = grid_smem(P->rows_cap, cs, cs.ldw, true);
+        const bool want_res = (d->flags & STO_PLAN_FORCE_RESIDENT) ||
+                              (!(d->flags & STO_PLAN_FORCE_STREAM) && res_smem <= kSmemBudget);
+        if (want_res) {
+            if (res_smem > kSmemBudget)
+                return bail(fail(STO_E_PARAM, "resident kernel does not fit shared memory"));
+            P->kind = kResident;
+            P->chunk_cols = cs.ldw;
+            P->smem = res_smem;
+        } else {
+            P->kind = kStream;
+            P->chunk_cols = choose_chunk(cs, P->rows_cap, false);
+            P->smem = grid_smem(P->rows_cap, cs, P->chunk_cols, false);
+            const double wbytes = (double)n * cs.ldw * sizeof(double);
+            P->stream_evict_first = wbytes > 0.6 * (double)P->l2_bytes;
+        }
+        P->grid = g;
+    }
+    *out = P;
+    return STO_OK;
+}
+
+void sto_plan_destroy(sto_plan *P) {
+    if (!P) return;
+    cudaSetDevice(P->device);
+    cudaFree(P->L.w);
+    cudaFree(P->w_in);
+    cudaFree(P->xbuf);
+    cudaFree(P->bar);
+    cudaFree(P->status);
+    delete P;
+}
+
+int sto_plan_get_info(const sto_plan *P, sto_plan_info *info) {
+    if (!P || !info) return fail(STO_E_PARAM, "null plan or info");
+    info->kernel = P->kind;
+    info->grid = P->grid;
+    info->threads = P->kind == kTiny ? 32 : kThreads;
+    info->smem_bytes = (int)P->smem;
+    info->ldw = P->L.cs.ldw;
+    info->block_cols = P->L.cs.blk;
+    info->w_bytes = (int64_t)P->n * P->L.cs.ldw * (int64_t)sizeof(double);
+    return STO_OK;
+}
+
+int sto_derivative(sto_plan *P, const double *m, const double *u, double *out, void *stream) {
+    if (!P || !m || !u || !out) return fail(STO_E_PARAM, "null argument");
+    STO_CUDA(cudaSetDevice(P->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    KParams p = base_params(P);
+    p.mode = kDerivative;
+    p.m = const_cast<double *>(m);
+    p.samples = u;
+    p.out = out;
+    const int g = std::min(P->sm_count, P->n);
+    p.rows_cap = (P->n + g - 1) / g;
+    p.chunk_cols = choose_chunk(P->L.cs, p.rows_cap, false);
+    const size_t smem = grid_smem(p.rows_cap, P->L.cs, p.chunk_cols, false);
+    return launch_grid<WSrc::GlobalL2, false>(p, g, smem, false, s);
+}
+
+int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *stream) {
+    if (!P || !r) return fail(STO_E_PARAM, "null plan or run");
+    if (!r->m || !r->samples || r->n_samples < 1 || r->steps_per_sample < 1 || r->steps < 1 ||
+        r->record_stride < 1 || !(r->dt > 0.0))
+        return fail(STO_E_PARAM, "bad run descriptor");
+    if (r->n_samples > 1 && !((r->n_samples - 1) * r->steps_per_sample < r->steps &&
+                              r->steps <= r->n_samples * r->steps_per_sample))
+        return fail(STO_E_PARAM, "input series does not cover the run (model.py:128-143)");
+    STO_CUDA(cudaSetDevice(P->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    KParams p = base_params(P);
+    p.mode = kIntegrate;
+    p.m = r->m;
+    p.samples = r->samples;
+    p.n_samples = r->n_samples;
+    p.sps = r->steps_per_sample;
+    p.dt = r->dt;
+    p.h2 = r->dt * 0.5;   // integrator.py:103
+    p.dt6 = r->dt / 6.0;  // integrator.py:104 (IEEE division, as in Python)
+    p.steps = r->steps;
+    p.stride = r->record_stride;
+    p.n_records = sto_n_records(r->steps, r->record_stride);
+    p.states = r->states;
+    p.rows_cap = P->rows_cap;
+    p.chunk_cols = P->chunk_cols;
+    reset_status_kernel<<<1, 1, 0, s>>>(P->status, P->bar);
+    STO_CUDA(cudaGetLastError());
+    int rc = STO_OK;
+    switch (P->kind) {
+        case kTiny: rc = launch_tiny(p, P->n, s); break;
+        case kSingle: rc = launch_grid<WSrc::Shared, true>(p, 1, P->smem, false, s); break;
+        case kResident: rc = launch_grid<WSrc::Shared, false>(p, P->grid, P->smem, true, s); break;
+        default:
+            rc = P->stream_evict_first
+                     ? launch_grid<WSrc::GlobalStream, false>(p, P->grid, P->smem, true, s)
+                     : launch_grid<WSrc::GlobalL2, false>(p, P->grid, P->smem, true, s);
+    }
+    if (rc) return rc;
+    if (status) return sto_plan_last_status(P, status, stream);
+    return STO_OK;
+}
+
+int sto_plan_last_status(sto_plan *P, sto_status *status, void *stream) {
+    if (!P || !status) return fail(STO_E_PARAM, "null plan or status");
+    STO_CUDA(cudaSetDevice(P->device));
+    StatusDev h{};
+    STO_CUDA(cudaMemcpyAsync(&h, P->status, sizeof(h), cudaMemcpyDeviceToHost,
+                             (cudaStream_t)stream));
+    STO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    status->diverged = h.flag;
+    status->reserved = 0;
+    status->oscillator = h.flag ? h.oscillator : -1;
+    status->step = h.flag ? h.step : -1;
+    if (h.flag)
+        return fail(STO_E_DIVERGED, "non-finite state for oscillator " +
+                                        std::to_string(h.oscillator) + " at step " +
+                                        std::to_string(h.step));
+    return STO_OK;
+}
+
+int sto_integrate_host(sto_plan *P, double *m, const double *samples, int64_t n_samples,
+                       int64_t steps_per_sample, double dt, int64_t steps, int64_t record_stride,
+                       double *states, sto_status *status) {
+    if (!P || !m || !samples || !states || !status) return fail(STO_E_PARAM, "null argument");
+    STO_CUDA(cudaSetDevice(P->device));
+    const int64_t nrec = sto_n_records(steps, record_stride);
+    if (nrec < 1 || n_samples < 1) return fail(STO_E_PARAM, "bad run sizes");
+    const size_t mb = sizeof(double) * 3 * (size_t)P->n;
+    const size_t sb = sizeof(double) * (size_t)n_samples * P->n_in;
+    double *dm = nullptr, *ds = nullptr, *dst = nullptr;
+    STO_CUDA(cudaMalloc(&dm, mb));
+    STO_CUDA(cudaMalloc(&ds, sb));
+    STO_CUDA(cudaMalloc(&dst, mb * nrec));
+    int rc = STO_OK;
+    if (cudaMemcpy(dm, m, mb, cudaMemcpyDefault) != cudaSuccess ||
+        cudaMemcpy(ds, samples, sb, cudaMemcpyDefault) != cudaSuccess) {
+        rc = fail(STO_E_CUDA, "host to device copy failed");
+    } else {
+        sto_run r{dm, ds, n_samples, steps_per_sample, dt, steps, record_stride, dst};
+        rc = sto_integrate(P, &r, status, nullptr);
+        if (rc == STO_OK || rc == STO_E_DIVERGED) {
+            const int keep = rc;
+            if (cudaMemcpy(states, dst, mb * nrec, cudaMemcpyDefault) != cudaSuccess ||
+                cudaMemcpy(m, dm, mb, cudaMemcpyDefault) != cudaSuccess)
+                rc = fail(STO_E_CUDA, "device to host copy failed");
+            else
+                rc = keep;
+        }
+    }
+    cudaFree(dm);
+    cudaFree(ds);
+    cudaFree(dst);
+    return rc;
+}
+
+int sto_tree_matvec(int device, int64_t rows, int64_t cols, const double *a, int64_t lda,
+                    const double *x, double *out) {
+    if (rows < 1 || cols < 1 || lda < cols || !a || !x || !out)
+        return fail(STO_E_PARAM, "bad matvec arguments");
+    cudaDeviceProp prop;
+    if (int rc = check_device(device, &prop)) return rc;
+    STO_CUDA(cudaSetDevice(device));
+    Layout L;
+    int rc = upload_layout(L, (int)rows, (int)cols, a, lda, cols >= 8192 ? 2048 : 512, nullptr);
+    double *dx = nullptr, *dout = nullptr;
+    if (rc == STO_OK) {
+        if (cudaMalloc(&dx, sizeof(double) * cols) != cudaSuccess ||
+            cudaMalloc(&dout, sizeof(double) * rows) != cudaSuccess ||
+            cudaMemcpy(dx, x, sizeof(double) * cols, cudaMemcpyDefault) != cudaSuccess) {
+            rc = fail(STO_E_CUDA, "matvec staging failed");
+        } else {
+            KParams p{};
+            p.cs = L.cs;
+            p.rows = (int)rows;
+            p.mode = kMatvec;
+            p.w = L.w;
+            p.xsrc = dx;
+            p.x_stride = 1;
+            p.out = dout;
+            const int g = (int)std::min<int64_t>(prop.multiProcessorCount, rows);
+            p.rows_cap = (int)((rows + g - 1) / g);
+            p.chunk_cols = choose_chunk(L.cs, p.rows_cap, false);
+            const size_t smem = grid_smem(p.rows_cap, L.cs, p.chunk_cols, false);
+            rc = launch_grid<WSrc::GlobalL2, false>(p, g, smem, false, nullptr);
+            if (rc == STO_OK &&
+                cudaMemcpy(out, dout, sizeof(double) * rows, cudaMemcpyDefault) != cudaSuccess)
+                rc = fail(STO_E_CUDA, "matvec result copy failed");
+        }
+    }
+    cudaFree(dx);
+    cudaFree(dout);
+    cudaFree(L.w);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,296 @@
+// sto_device.cuh -- device-side building blocks of the coupled-STO RK4 path.
+//
+// Bit-exactness contract (SURVEY §8(a), §7 "hard parts"):
+//  * every product and sum is rounded separately: the arithmetic below goes
+//    through __dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn (which ptxas never
+//    contracts into DFMA) and the library is also built with -fmad=false;
+//  * operation order is the reference's pinned order: row_rhs() restates
+//    backends/cpu_jit.py:62-87 (== model.py:239-301), the RK4 combination
+//    restates integrator.py:100-121;
+//  * row sums use the reference's adjacent-pairs tree (model.py:31-52,
+//    cpu_jit.py:28-45), which equals the aligned power-of-two tree over the
+//    row padded with -0.0 (the exact additive identity of IEEE round-to-
+//    nearest, so padding never changes a bit, signed zeros included).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sto {
+
+// ----------------------------------------------------------------------------
+// strict IEEE scalar helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double fmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double fsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double fdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+struct Consts {
+    double c_prec, c_damp, h_appl, h_aniso, pref, lam, a_cp, a_in, px, py, pz;
+};
+
+struct V3 {
+    double x, y, z;
+};
+
+// dm/dt of one oscillator given its coupling row sum `cp` and input row sum
+// `cin`.  cpu_jit.py:62-87 / model.py:239-301, operation for operation.
+__device__ __forceinline__ V3 row_rhs(V3 m, double cp, double cin, const Consts &c) {
+    double md = fadd(fmul(m.x, c.px), fmul(m.y, c.py));
+    md = fadd(md, fmul(m.z, c.pz));
+    const double hs = fdiv(c.pref, fadd(1.0, fmul(c.lam, md)));
+
+    const double qx = fsub(fmul(c.py, m.z), fmul(c.pz, m.y));
+    const double qy = fsub(fmul(c.pz, m.x), fmul(c.px, m.z));
+    const double qz = fsub(fmul(c.px, m.y), fmul(c.py, m.x));
+
+    const double bx = fadd(fadd(fmul(c.a_cp, cp), fmul(c.a_in, cin)), fmul(hs, qx));
+    const double by = fmul(hs, qy);
+    const double bz = fadd(fadd(c.h_appl, fmul(c.h_aniso, m.z)), fmul(hs, qz));
+
+    const double ax = fsub(fmul(m.y, bz), fmul(m.z, by));
+    const double ay = fsub(fmul(m.z, bx), fmul(m.x, bz));
+    const double az = fsub(fmul(m.x, by), fmul(m.y, bx));
+
+    const double ex = fsub(fmul(m.y, az), fmul(m.z, ay));
+    const double ey = fsub(fmul(m.z, ax), fmul(m.x, az));
+    const double ez = fsub(fmul(m.x, ay), fmul(m.y, ax));
+
+    V3 d;
+    d.x = fsub(-fmul(c.c_prec, ax), fmul(c.c_damp, ex));
+    d.y = fsub(-fmul(c.c_prec, ay), fmul(c.c_damp, ey));
+    d.z = fsub(-fmul(c.c_prec, az), fmul(c.c_damp, ez));
+    return d;
+}
+
+// s = m + k*h   (integrator.py:107-108, 110-111, 113-114)
+__device__ __forceinline__ V3 stage_point(V3 m, V3 k, double h) {
+    return V3{fadd(m.x, fmul(k.x, h)), fadd(m.y, fmul(k.y, h)), fadd(m.z, fmul(k.z, h))};
+}
+
+// acc = k1 + k2*2   (integrator.py:117-118)
+__device__ __forceinline__ V3 acc_k2(V3 k1, V3 k2) {
+    return V3{fadd(k1.x, fmul(k2.x, 2.0)), fadd(k1.y, fmul(k2.y, 2.0)),
+              fadd(k1.z, fmul(k2.z, 2.0))};
+}
+
+// m + ((acc + (k3*2 + k4)) * dt_6)   (integrator.py:119-121)
+__device__ __forceinline__ V3 rk4_final(V3 m, V3 acc, V3 k3, V3 k4, double dt6) {
+    V3 r;
+    r.x = fadd(m.x, fmul(fadd(acc.x, fadd(fmul(k3.x, 2.0), k4.x)), dt6));
+    r.y = fadd(m.y, fmul(fadd(acc.y, fadd(fmul(k3.y, 2.0), k4.y)), dt6));
+    r.z = fadd(m.z, fmul(fadd(acc.z, fadd(fmul(k3.z, 2.0), k4.z)), dt6));
+    return r;
+}
+
+__device__ __forceinline__ bool all_finite(V3 m) {
+    return isfinite(m.x) && isfinite(m.y) && isfinite(m.z);
+}
+
+// Pinned adjacent-pairs tree of a[i]*b[i], i < w, streamed with a carry stack
+// (binary counter): each completed aligned subtree is merged left+right as
+// soon as its right sibling completes; the final fold adds the incomplete
+// right edge (the padded region) exactly as the odd-tail carry does.
+__device__ __forceinline__ double tree_dot_stream(const double *a, const double *b, int w) {
+    double stk[32];
+    unsigned cnt = 0;
+    for (int i = 0; i < w; ++i) {
+        double v = fmul(a[i], b[i]);
+        int lvl = 0;
+        while (cnt & (1u << lvl)) {
+            v = fadd(stk[lvl], v);
+            ++lvl;
+        }
+        stk[lvl] = v;
+        ++cnt;
+    }
+    double acc = 0.0;
+    bool have = false;
+    for (int lvl = 0; lvl < 32; ++lvl) {
+        if (cnt & (1u << lvl)) {
+            acc = have ? fadd(stk[lvl], acc) : stk[lvl];
+            have = true;
+        }
+    }
+    return acc;
+}
+
+// In-place adjacent-pairs tree over buf[0:w] (cpu_jit.py:28-45 verbatim order).
+__device__ __forceinline__ double tree_inplace(double *buf, int w) {
+    while (w > 1) {
+        const int half = w >> 1;
+        for (int j = 0; j < half; ++j) buf[j] = fadd(buf[2 * j], buf[2 * j + 1]);
+        if (w & 1) {
+            buf[half] = buf[w - 1];
+            w = half + 1;
+        } else {
+            w = half;
+        }
+    }
+    return buf[0];
+}
+
+// ----------------------------------------------------------------------------
+// Column schedule of the device W layout ("lane-blocked" segments).
+//
+// A row is cut into segments of S = 32*C columns, C a power of two: first
+// `nfull` segments of 512 (C = 16), then a tail of decreasing sizes from
+// {256, 128, 64} plus one zero-padded 64 segment for the last < 64 columns.
+// Sizes never increase, so every segment is an aligned node of the padded
+// power-of-two tree.  Inside a segment, lane l owns the C contiguous
+// columns [l*C, (l+1)*C); they are stored so that a warp-wide 16-byte load
+// i delivers columns l*C + 2i, +1 to lane l:
+//     offset(l, q) = ((q >> 1) * 32 + l) * 2 + (q & 1)
+// Hence every load is perfectly coalesced (512 B per warp instruction), each
+// lane reduces its chunk in registers, and a 5-level xor butterfly finishes
+// the segment node -- all in the reference's tree order.
+// ----------------------------------------------------------------------------
+constexpr int kSegFull = 512;
+constexpr int kMaxTail = 4;
+constexpr int kMaxLeaves = 8;  // block_cols / 512 <= 8
+
+struct ColSched {
+    int n;        // real columns
+    int ldw;      // padded physical width
+    int nfull;    // 512-column segments
+    int ntail;    // tail segments
+    int tail_base[kMaxTail];
+    int tail_c[kMaxTail];  // columns per lane in each tail segment
+    int blk;      // columns per work block (512 * 2^r, r <= 3)
+    int nblocks;  // ceil(ldw / blk)
+};
+
+__host__ __device__ inline int seg_offset(int l, int q) { return (((q >> 1) << 5) + l) * 2 + (q & 1); }
+
+// physical position of logical column k
+__host__ __device__ inline int col_perm(const ColSched &s, int k) {
+    if (k < s.nfull * kSegFull) {
+        const int q = k & (kSegFull - 1);
+        return (k & ~(kSegFull - 1)) + seg_offset(q >> 4, q & 15);
+    }
+    for (int t = 0; t < s.ntail; ++t) {
+        const int c = s.tail_c[t];
+        const int base = s.tail_base[t];
+        if (k < base + 32 * c) {
+            const int q = k - base;
+            return base + seg_offset(q / c, q % c);
+        }
+    }
+    return -1;
+}
+
+// Load policies for W.
+enum class WSrc { Shared, GlobalL2, GlobalStream };
+
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+template <WSrc S>
+__device__ __forceinline__ double2 load_w2(const double *p) {
+    if constexpr (S == WSrc::Shared) {
+        return *reinterpret_cast<const double2 *>(p);
+    } else {
+        const uint64_t pol = (S == WSrc::GlobalL2) ? l2_policy_evict_last() : l2_policy_evict_first();
+        double2 v;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                     : "=d"(v.x), "=d"(v.y)
+                     : "l"(p), "l"(pol));
+        return v;
+    }
+}
+
+// Node of one segment (32*C columns).  wseg/xseg point at the segment start
+// of the W row and of the staged X vector (same layout).
+template <int C, WSrc S>
+__device__ __forceinline__ double segment_node(const double *wseg, const double *xseg, int lane) {
+    double p[C];
+#pragma unroll
+    for (int i = 0; i < C / 2; ++i) {
+        const double2 w = load_w2<S>(wseg + ((i << 5) + lane) * 2);
+        const double2 x = *reinterpret_cast<const double2 *>(xseg + ((i << 5) + lane) * 2);
+        p[2 * i] = fmul(w.x, x.x);
+        p[2 * i + 1] = fmul(w.y, x.y);
+    }
+#pragma unroll
+    for (int w = C; w > 1; w >>= 1) {
+#pragma unroll
+        for (int j = 0; j < w / 2; ++j) p[j] = fadd(p[2 * j], p[2 * j + 1]);
+    }
+    double v = p[0];
+#pragma unroll
+    for (int mask = 1; mask < 32; mask <<= 1) v = fadd(v, __shfl_xor_sync(0xffffffffu, v, mask));
+    return v;
+}
+
+template <WSrc S>
+__device__ __forceinline__ double tail_segment_node(int c, const double *wseg, const double *xseg,
+                                                    int lane) {
+    switch (c) {
+        case 8: return segment_node<8, S>(wseg, xseg, lane);
+        case 4: return segment_node<4, S>(wseg, xseg, lane);
+        default: return segment_node<2, S>(wseg, xseg, lane);
+    }
+}
+
+// Node of one work block [b*blk, (b+1)*blk) of one row: its full 512-segment
+// nodes are leaves; the tail (if the block holds it) is folded right to left
+// (sizes decrease, so T = S0 + (S1 + (... + Sk))) into one 512-level leaf;
+// the leaves then go through the pinned pairwise tree (width <= 8).
+// wrow/xrow point at column 0 of the row / of the X window (x_base = first
+// physical column held in the X window).
+template <WSrc S>
+__device__ __forceinline__ double block_node(const ColSched &cs, int b, const double *wrow,
+                                             const double *xwin, int x_base, int lane) {
+    const int c0 = b * cs.blk;
+    const int seg0 = c0 / kSegFull;
+    const int per = cs.blk / kSegFull;
+    int nf = cs.nfull - seg0;
+    nf = nf < 0 ? 0 : (nf > per ? per : nf);
+    const bool has_tail = cs.ntail > 0 && cs.tail_base[0] >= c0 && cs.tail_base[0] < c0 + cs.blk;
+
+    double leaf[kMaxLeaves];
+#pragma unroll
+    for (int j = 0; j < kMaxLeaves; ++j) {
+        if (j < nf) {
+            const int col = (seg0 + j) * kSegFull;
+            leaf[j] = segment_node<16, S>(wrow + col, xwin + (col - x_base), lane);
+        }
+    }
+    int width = nf;
+    if (has_tail) {
+        double t = 0.0;
+        for (int k = cs.ntail - 1; k >= 0; --k) {
+            const int col = cs.tail_base[k];
+            const double v = tail_segment_node<S>(cs.tail_c[k], wrow + col, xwin + (col - x_base), lane);
+            t = (k == cs.ntail - 1) ? v : fadd(v, t);
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxLeaves; ++j)
+            if (j == nf) leaf[j] = t;
+        width = nf + 1;
+    }
+    // pinned pairwise tree over leaf[0:width], compile-time register indices
+#pragma unroll
+    for (int lvl = 0; lvl < 3; ++lvl) {
+#pragma unroll
+        for (int j = 0; j < (kMaxLeaves >> (lvl + 1)); ++j) {
+            if (2 * j + 1 < width)
+                leaf[j] = fadd(leaf[2 * j], leaf[2 * j + 1]);
+            else if (2 * j < width)
+                leaf[j] = leaf[2 * j];
+        }
+        width = (width + 1) >> 1;
+    }
+    return leaf[0];
+}
+
+}  // namespace sto

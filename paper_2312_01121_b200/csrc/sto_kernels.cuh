@@ -1,0 +1,404 @@
+// sto_kernels.cuh -- the persistent RK4 kernels (one launch per integrate()).
+//
+//   tiny_rk4_kernel<NMAX>   n <= 32: one warp, lane k owns oscillator k, W row
+//                            in registers, x-exchange through shared memory.
+//   grid_rk4_kernel<S,SINGLE>  general n: CTAs own contiguous row blocks; each
+//                            RK stage = block phase (warps compute (row, column
+//                            block) tree nodes of W.x) + row phase (one thread
+//                            per oscillator: row fold, input field, LLG RHS, RK4
+//                            stage update, x publication, recording) + one
+//                            exchange of the stage x-vector (grid barrier over a
+//                            double-buffered global x, or __syncthreads when
+//                            SINGLE).  W is read from shared memory (resident),
+//                            from L2 (evict_last) or streamed from HBM
+//                            (evict_first) according to S.
+// The same grid kernel evaluates one derivative (mode 1, K0) and a plain
+// pinned-tree matvec (mode 2).
+#pragma once
+
+#include "sto_device.cuh"
+
+namespace sto {
+
+struct StatusDev {
+    int32_t flag;
+    int32_t pad;
+    long long oscillator;
+    long long step;
+};
+
+enum KernelMode : int { kIntegrate = 0, kDerivative = 1, kMatvec = 2 };
+
+struct KParams {
+    ColSched cs;
+    Consts c;
+    int rows;               // oscillators (rows of W)
+    int n_in;
+    int mode;
+    int rows_cap;           // max rows per CTA (shared-memory sizing)
+    int chunk_cols;         // X window width in physical columns (multiple of blk)
+    const double *w;        // rows x ldw, device layout
+    const double *w_in;     // rows x n_in
+    double *m;              // (rows, 3): initial state in / final out; (mode 1) state
+    int x_stride;           // stride of the x source for mode 2 (vector) == 1
+    const double *xsrc;     // mode 2: x vector (cols)
+    const double *samples;  // (n_samples, n_in); mode 1: u
+    long long n_samples, sps;
+    double dt, h2, dt6;
+    long long steps, stride, n_records;
+    double *states;         // (n_records, rows, 3) or null
+    double *out;            // mode 1: (rows,3); mode 2: (rows)
+    double *xbuf;           // 2 x ldw published stage x (physical layout), +0.0 padded
+    unsigned long long *bar;
+    StatusDev *status;
+};
+
+// ----------------------------------------------------------------------------
+// grid-wide barrier (release/acquire at gpu scope; co-residency guaranteed by
+// cooperative launch).  `target` = epoch * gridDim.x.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long long target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+        } while (v < target);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double ld_cg(const double *p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double2 ld_cg2(const double *p) {
+    double2 v;
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ int row_lo(int b, int g, int rows) {
+    return (int)(((long long)b * rows) / g);
+}
+
+__device__ __forceinline__ long long record_index(long long step, long long stride,
+                                                  long long steps, long long n_records) {
+    if (step % stride == 0) return step / stride;
+    return step == steps ? n_records - 1 : -1;
+}
+
+// Per-row RK state in shared memory (13 doubles per local row).
+struct RowState {
+    double *base;
+    int cap;
+    __device__ V3 get(int slot, int r) const {
+        const double *p = base + (slot * 3) * cap;
+        return V3{p[r], p[cap + r], p[2 * cap + r]};
+    }
+    __device__ void put(int slot, int r, V3 v) const {
+        double *p = base + (slot * 3) * cap;
+        p[r] = v.x;
+        p[cap + r] = v.y;
+        p[2 * cap + r] = v.z;
+    }
+    __device__ double &cin(int r) const { return base[12 * cap + r]; }
+};
+enum { kSlotM = 0, kSlotS = 1, kSlotAcc = 2, kSlotK3 = 3 };
+
+// Shared layout: [X window | W rows (resident) | nodes | row state | flags]
+template <WSrc S, bool SINGLE>
+__global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant__ KParams p) {
+    extern __shared__ __align__(16) double smem[];
+    const ColSched &cs = p.cs;
+    const int G = gridDim.x;
+    const int b = blockIdx.x;
+    const int r0 = row_lo(b, G, p.rows);
+    const int nrow = row_lo(b + 1, G, p.rows) - r0;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+
+    double *xs = smem;
+    double *wres = xs + p.chunk_cols;
+    const size_t wres_sz = (S == WSrc::Shared) ? (size_t)p.rows_cap * cs.ldw : 0;
+    double *nodes = wres + wres_sz;
+    RowState rs{nodes + (size_t)p.rows_cap * cs.nblocks, p.rows_cap};
+    volatile int *sflag = reinterpret_cast<volatile int *>(rs.base + 13 * p.rows_cap);
+
+    // ---- prologue: resident W rows, own state, initial record -------------
+    if constexpr (S == WSrc::Shared) {
+        const double2 *src = reinterpret_cast<const double2 *>(p.w + (size_t)r0 * cs.ldw);
+        double2 *dst = reinterpret_cast<double2 *>(wres);
+        const int n2 = nrow * cs.ldw / 2;
+        for (int i = threadIdx.x; i < n2; i += blockDim.x) dst[i] = src[i];
+    }
+    const bool integrate = p.mode == kIntegrate;
+    if (p.mode != kMatvec) {
+        for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
+            const double *mm = p.m + 3 * (size_t)(r0 + r);
+            const V3 v{mm[0], mm[1], mm[2]};
+            rs.put(kSlotM, r, v);
+            if (integrate && p.states) {
+                double *st = p.states + 3 * (size_t)(r0 + r);
+                st[0] = v.x;
+                st[1] = v.y;
+                st[2] = v.z;
+            }
+        }
+    }
+    if (threadIdx.x == 0) *sflag = 0;
+    __syncthreads();
+
+    const long long total_stages = integrate ? 4 * p.steps : 1;
+    const int nchunks = (cs.ldw + p.chunk_cols - 1) / p.chunk_cols;
+    const int blocks_per_chunk = p.chunk_cols / cs.blk;
+    const double *u = p.samples;
+
+    for (long long e = 0; e < total_stages; ++e) {
+        const int stage = (int)(e & 3);
+        const long long step = (e >> 2) + 1;
+        // ---------------- block phase: tree nodes of W . x ----------------
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int x_base = ch * p.chunk_cols;
+            const int x_len = min(p.chunk_cols, cs.ldw - x_base);
+            if (!SINGLE || e == 0) {
+                if (e == 0) {
+                    // initial x from the state (or the matvec vector): scatter
+                    // logical columns into the physical layout, +0.0 padding
+                    for (int i = threadIdx.x; i < x_len; i += blockDim.x) xs[i] = 0.0;
+                    __syncthreads();
+                    const int k_end = min(cs.n, x_base + x_len);
+                    for (int k = x_base + threadIdx.x; k < k_end; k += blockDim.x) {
+                        const double v = (p.mode == kMatvec) ? p.xsrc[(size_t)k * p.x_stride]
+                                                             : p.m[3 * (size_t)k];
+                        xs[col_perm(cs, k) - x_base] = v;
+                    }
+                } else {
+                    const double *src = p.xbuf + (size_t)(e & 1) * cs.ldw + x_base;
+                    for (int i = 2 * threadIdx.x; i < x_len; i += 2 * blockDim.x) {
+                        const double2 v = ld_cg2(src + i);
+                        xs[i] = v.x;
+                        xs[i + 1] = v.y;
+                    }
+                }
+                __syncthreads();
+            }
+            const int bfirst = ch * blocks_per_chunk;
+            const int bcount = min(blocks_per_chunk, cs.nblocks - bfirst);
+            const int units = nrow * bcount;
+            for (int unit = warp; unit < units; unit += nwarps) {
+                const int r = unit / bcount;
+                const int bb = bfirst + unit % bcount;
+                const double *wrow = (S == WSrc::Shared) ? wres + (size_t)r * cs.ldw
+                                                         : p.w + (size_t)(r0 + r) * cs.ldw;
+                const double node = block_node<S>(cs, bb, wrow, xs, x_base, lane);
+                if (lane == 0) nodes[(size_t)r * cs.nblocks + bb] = node;
+            }
+            __syncthreads();
+        }
+        // ---------------- row phase: RHS + RK4 stage update ----------------
+        const long long rec = (integrate && stage == 3)
+                                  ? record_index(step, p.stride, p.steps, p.n_records)
+                                  : -1;
+        double *xnext = SINGLE ? xs : p.xbuf + (size_t)((e + 1) & 1) * cs.ldw;
+        for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
+            const int k = r0 + r;
+            const double cp = tree_inplace(nodes + (size_t)r * cs.nblocks, cs.nblocks);
+            if (p.mode == kMatvec) {
+                p.out[k] = cp;
+                continue;
+            }
+            if (stage == 0) {
+                rs.cin(r) = (p.n_in == 1)
+                                ? fmul(p.w_in[k], u[0])
+                                : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
+            }
+            const V3 mk = rs.get(kSlotM, r);
+            const V3 cur = (stage == 0) ? mk : rs.get(kSlotS, r);
+            const V3 d = row_rhs(cur, cp, rs.cin(r), p.c);
+            if (!integrate) {
+                double *o = p.out + 3 * (size_t)k;
+                o[0] = d.x;
+                o[1] = d.y;
+                o[2] = d.z;
+                continue;
+            }
+            double xpub;
+            if (stage == 0) {
+                rs.put(kSlotAcc, r, d);
+                const V3 s = stage_point(mk, d, p.h2);
+                rs.put(kSlotS, r, s);
+                xpub = s.x;
+            } else if (stage == 1) {
+                rs.put(kSlotAcc, r, acc_k2(rs.get(kSlotAcc, r), d));
+                const V3 s = stage_point(mk, d, p.h2);
+                rs.put(kSlotS, r, s);
+                xpub = s.x;
+            } else if (stage == 2) {
+                rs.put(kSlotK3, r, d);
+                const V3 s = stage_point(mk, d, p.dt);
+                rs.put(kSlotS, r, s);
+                xpub = s.x;
+            } else {
+                const V3 mn = rk4_final(mk, rs.get(kSlotAcc, r), rs.get(kSlotK3, r), d, p.dt6);
+                rs.put(kSlotM, r, mn);
+                xpub = mn.x;
+                if (rec >= 0) {
+                    if (!all_finite(mn)) {
+                        atomicMin(&p.status->oscillator, (long long)k);
+                        p.status->step = step;
+                        p.status->flag = 1;
+                        *sflag = 1;
+                    } else if (p.states) {
+                        double *st = p.states + ((size_t)rec * p.rows + k) * 3;
+                        st[0] = mn.x;
+                        st[1] = mn.y;
+                        st[2] = mn.z;
+                    }
+                }
+            }
+            xnext[col_perm(cs, k)] = xpub;
+        }
+        if (!integrate) break;
+        if (e + 1 == total_stages) break;
+        // ---------------- exchange of the stage x-vector ----------------
+        if constexpr (SINGLE) {
+            __syncthreads();
+            if (*sflag) break;
+        } else {
+            grid_sync(p.bar, (unsigned long long)(e + 1) * G);
+            if (stage == 3 && rec >= 0) {
+                if (threadIdx.x == 0) *sflag = *((volatile int32_t *)&p.status->flag);
+                __syncthreads();
+                if (*sflag) break;
+            }
+        }
+        if (stage == 3) {
+            // next step's drive sample (zero-order hold, integrator.py:172)
+            const long long nxt = step;  // 0-based index of the next step
+            const long long idx = p.n_samples == 1 ? 0 : nxt / p.sps;
+            u = p.samples + idx * p.n_in;
+        }
+    }
+    // ---- epilogue: final state back to m -----------------------------------
+    if (integrate) {
+        __syncthreads();
+        for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
+            const V3 v = rs.get(kSlotM, r);
+            double *mm = p.m + 3 * (size_t)(r0 + r);
+            mm[0] = v.x;
+            mm[1] = v.y;
+            mm[2] = v.z;
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// n <= 32: one warp, everything in registers; shared memory only carries the
+// published stage x between lanes.  NMAX = smallest power of two >= n.
+// ----------------------------------------------------------------------------
+template <int NMAX>
+__global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__ KParams p) {
+    __shared__ double xsh[NMAX > 1 ? NMAX : 1];
+    const int k = threadIdx.x;
+    const int n = p.rows;
+    const bool live = k < n;
+    const Consts &c = p.c;
+    double w[NMAX];
+    V3 m{0.0, 0.0, 0.0};
+    if (live) {
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) w[j] = (j < n) ? p.w[(size_t)k * p.cs.ldw + col_perm(p.cs, j)] : 0.0;
+        m = V3{p.m[3 * k], p.m[3 * k + 1], p.m[3 * k + 2]};
+        if (p.states) {
+            p.states[3 * k] = m.x;
+            p.states[3 * k + 1] = m.y;
+            p.states[3 * k + 2] = m.z;
+        }
+    }
+    // coupling row sum at the current published x (pinned pairwise tree)
+    auto coupling = [&](double xown) -> double {
+        if constexpr (NMAX == 1) {
+            return fmul(w[0], xown);
+        } else {
+            double t[NMAX];
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) t[j] = (j < n) ? fmul(w[j], xsh[j]) : 0.0;
+            int width = n;
+#pragma unroll
+            for (int half = NMAX / 2; half >= 1; half >>= 1) {
+#pragma unroll
+                for (int j = 0; j < half; ++j) {
+                    if (2 * j + 1 < width)
+                        t[j] = fadd(t[2 * j], t[2 * j + 1]);
+                    else if (2 * j < width)
+                        t[j] = t[2 * j];
+                }
+                width = (width + 1) >> 1;
+            }
+            return t[0];
+        }
+    };
+    auto publish = [&](double x) {
+        if constexpr (NMAX > 1) {
+            __syncwarp();
+            if (live) xsh[k] = x;
+            __syncwarp();
+        }
+    };
+    publish(m.x);
+    int diverged = 0;
+    for (long long step = 1; step <= p.steps; ++step) {
+        const long long idx = p.n_samples == 1 ? 0 : (step - 1) / p.sps;
+        const double *u = p.samples + idx * p.n_in;
+        double cin = 0.0;
+        if (live)
+            cin = (p.n_in == 1) ? fmul(p.w_in[k], u[0])
+                                : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
+        const V3 k1 = row_rhs(m, coupling(m.x), cin, c);
+        V3 s = stage_point(m, k1, p.h2);
+        publish(s.x);
+        const V3 k2 = row_rhs(s, coupling(s.x), cin, c);
+        const V3 acc = acc_k2(k1, k2);
+        s = stage_point(m, k2, p.h2);
+        publish(s.x);
+        const V3 k3 = row_rhs(s, coupling(s.x), cin, c);
+        s = stage_point(m, k3, p.dt);
+        publish(s.x);
+        const V3 k4 = row_rhs(s, coupling(s.x), cin, c);
+        m = rk4_final(m, acc, k3, k4, p.dt6);
+        publish(m.x);
+        const long long rec = record_index(step, p.stride, p.steps, p.n_records);
+        if (rec >= 0) {
+            const bool bad = live && !all_finite(m);
+            const unsigned badmask = __ballot_sync(0xffffffffu, bad);
+            if (badmask) {
+                if (k == 0) {
+                    p.status->oscillator = __ffs(badmask) - 1;
+                    p.status->step = step;
+                    p.status->flag = 1;
+                }
+                diverged = 1;
+                break;
+            }
+            if (live && p.states) {
+                double *st = p.states + ((size_t)rec * n + k) * 3;
+                st[0] = m.x;
+                st[1] = m.y;
+                st[2] = m.z;
+            }
+        }
+    }
+    if (live && !diverged) {
+        p.m[3 * k] = m.x;
+        p.m[3 * k + 1] = m.y;
+        p.m[3 * k + 2] = m.z;
+    }
+}
+
+}  // namespace sto

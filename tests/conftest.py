@@ -1,0 +1,59 @@
+"""Shared fixtures.  `gpu` marks tests that need a B200 (run on the GPU box)."""
+
+from __future__ import annotations
+
+import glob
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs an sm_100 GPU and libsto_b200.so")
+
+
+def load_golden(name: str) -> dict:
+    with np.load(GOLDEN / name, allow_pickle=False) as z:
+        return {k: z[k] for k in z.files}
+
+
+def golden_trajectories() -> list[str]:
+    return sorted(os.path.basename(p) for p in glob.glob(str(GOLDEN / "traj_*.npz")))
+
+
+def bits(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64)).view(np.uint64)
+
+
+def assert_bit_equal(got, want, what: str = "") -> None:
+    got, want = np.asarray(got), np.asarray(want)
+    assert got.shape == want.shape, f"{what}: shape {got.shape} vs {want.shape}"
+    if not np.array_equal(bits(got), bits(want)):
+        diff = np.abs(got - want)
+        idx = np.unravel_index(np.nanargmax(np.where(np.isnan(diff), 0, diff)), diff.shape)
+        nbad = int((bits(got) != bits(want)).sum())
+        raise AssertionError(f"{what}: {nbad} values differ in bits; max |diff| "
+                             f"{diff[idx]:.3e} at {idx}")
+
+
+@pytest.fixture(scope="session")
+def params():
+    from paper_2312_01121_b200 import PhysicalParams
+
+    return PhysicalParams()
+
+
+@pytest.fixture(scope="session")
+def oracle_mod():
+    from oracle import oracle
+
+    oracle.build()
+    return oracle

@@ -1,0 +1,256 @@
+"""Host-side mirror of the reference API (no GPU needed).
+
+Parameters, topology construction (pinned bit-exactly against W matrices the
+reference built), drive series, run configuration, recording grid, the
+backend registry and the stage-wise path for derivative-only plugins --
+modelled on the reference's own test_params / test_topology / test_model /
+test_integrator / test_backends suites.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2312_01121_b200 as sto
+from paper_2312_01121_b200 import (BackendUnavailableError, InputSeries,
+                                   IntegrationDivergedError, ParameterError, PhysicalParams,
+                                   RunConfig, Topology, TrajectoryMismatchError,
+                                   compare_trajectories, integrate)
+from paper_2312_01121_b200.integrator import RK4Scratch, _recorded_steps, rk4_step
+from paper_2312_01121_b200.topology import (CouplingMatrix, InputWeights, RngStream,
+                                            build_topology, initial_state, spectral_radius)
+
+from conftest import assert_bit_equal, load_golden
+
+
+# ---------------------------------------------------------------- params ----
+def test_derived_constants_match_reference_freeze():
+    d = sto.derive(PhysicalParams())
+    # frozen in the reference's test_params.py:15-19
+    assert d.c_prec == pytest.approx(17639559.011024725, rel=1e-15)
+    assert d.c_damp == pytest.approx(88197.79505512363, rel=1e-15)
+    assert d.h_aniso == pytest.approx(416.12543922361147, rel=1e-15)
+    assert d.h_s_prefactor == pytest.approx(134.86812645902467, rel=1e-15)
+    assert sto.small_angle_frequency(PhysicalParams()) == pytest.approx(1.729767978589695e9,
+                                                                        rel=1e-12)
+
+
+def test_kernel_scalars_bit_equal_reference_pack():
+    # consts stored by make_golden.py come from the reference's _scalar_pack
+    z = load_golden("deriv.npz")
+    assert_bit_equal(np.array(sto.kernel_scalars(PhysicalParams())), z["consts"])
+    d = load_golden("traj_n160_params.npz")
+    p = PhysicalParams(alpha=0.01, current=3.0e-3, a_cp=2.0, a_in=0.5)
+    assert_bit_equal(np.array(sto.kernel_scalars(p)), d["consts"])
+
+
+@pytest.mark.parametrize("kwargs", [{"gamma": 0.0}, {"alpha": -1e-3}, {"lambda_stt": 1.0},
+                                    {"h_appl": float("nan")}, {"current": float("inf")},
+                                    {"p_vec": (0.0, 0.0, 0.0)}, {"volume": -1.0}])
+def test_params_validation(kwargs):
+    with pytest.raises(ParameterError):
+        PhysicalParams(**kwargs)
+
+
+# -------------------------------------------------------------- topology ----
+@pytest.mark.parametrize("n,n_in,seed", [(1, 1, 0), (2, 1, 1), (3, 1, 3), (6, 2, 5), (7, 1, 11),
+                                         (13, 1, 7), (33, 3, 33), (100, 1, 0), (160, 1, 3)])
+def test_build_topology_bit_equal_reference(n, n_in, seed):
+    ref = load_golden(f"topo_n{n}_in{n_in}_s{seed}.npz")
+    top = build_topology(n, n_in=n_in, seed=seed)
+    assert_bit_equal(top.coupling.entries, ref["w"], "W")
+    assert_bit_equal(top.input_weights.entries, ref["w_in"], "W_in")
+
+
+def test_rng_frozen_draws():
+    # reference test_topology.py:36-42
+    want = np.array([0.2739233746429086, -0.4604265724722594, -0.9180529521276106,
+                     -0.9669447289429418])
+    assert np.array_equal(RngStream(0).uniform_pm1(4), want)
+
+
+def test_spectral_radius_cases():
+    assert spectral_radius(np.array([[0.0, 0.7], [-0.3, 0.0]])) == pytest.approx(math.sqrt(0.21))
+    assert spectral_radius(np.zeros((6, 6))) == 0.0
+    shift = np.zeros((8, 8))
+    shift[np.arange(7), np.arange(1, 8)] = 1.0
+    assert spectral_radius(shift) == 0.0
+    g = np.random.default_rng(4)
+    w = g.uniform(-1, 1, (40, 40))
+    assert spectral_radius(w) == pytest.approx(np.abs(np.linalg.eigvals(w)).max(), rel=1e-8)
+
+
+def test_containers_validate():
+    with pytest.raises(ParameterError):
+        CouplingMatrix(entries=np.ones((2, 2)))
+    with pytest.raises(ParameterError):
+        InputWeights(entries=np.full((2, 1), 1.5))
+    with pytest.raises(ParameterError):
+        Topology(CouplingMatrix.zeros(3), InputWeights.zeros(4))
+    t = Topology.decoupled(5, n_in=2)
+    assert (t.n, t.n_in) == (5, 2)
+
+
+def test_initial_state_unit_norm():
+    m = initial_state(4)
+    assert m.shape == (4, 3)
+    assert np.allclose(np.linalg.norm(m, axis=1), 1.0, atol=1e-15)
+
+
+# ------------------------------------------------------------ drive/config ----
+def test_input_series_hold_and_bounds():
+    s = InputSeries(samples=np.array([[1.0], [2.0], [3.0]]), steps_per_sample=4)
+    assert [s.sample_for_step(i)[0] for i in range(12)] == [1.0] * 4 + [2.0] * 4 + [3.0] * 4
+    s.check_steps(9)
+    s.check_steps(12)
+    for bad in (8, 13):
+        with pytest.raises(ParameterError):
+            s.check_steps(bad)
+    with pytest.raises(ParameterError):
+        InputSeries(samples=np.array([[np.inf]]))
+
+
+@pytest.mark.parametrize("kwargs", [{"n": 0, "steps": 1, "dt": 1e-11},
+                                    {"n": 1, "steps": 0, "dt": 1e-11},
+                                    {"n": 1, "steps": 1, "dt": 0.0},
+                                    {"n": 1, "steps": 1, "dt": float("inf")},
+                                    {"n": 1, "steps": 1, "dt": 1e-11, "record_stride": 0},
+                                    {"n": 1, "steps": 1, "dt": 1e-11, "workers": 0}])
+def test_run_config_rejects(kwargs):
+    with pytest.raises(ParameterError):
+        RunConfig(**kwargs)
+
+
+def test_recording_grid():
+    assert list(_recorded_steps(5, 1)) == [0, 1, 2, 3, 4, 5]
+    assert list(_recorded_steps(10, 3)) == [0, 3, 6, 9, 10]
+    assert list(_recorded_steps(5, 100)) == [0, 5]
+
+
+# -------------------------------------------------------------- registry ----
+def test_registry_lists_gpu_backend():
+    ids = [d.backend_id for d in sto.list_backends()]
+    assert ids == ["gpu"]
+
+
+def test_unknown_backend_raises_listing_alternatives(params):
+    with pytest.raises(BackendUnavailableError) as info:
+        sto.create_backend("quantum", Topology.decoupled(1), params)
+    assert info.value.requested == "quantum"
+
+
+def test_register_replace_unregister(params):
+    class Zero:
+        def derivative(self, m, u, out):
+            out.fill(0.0)
+            return out
+
+    sto.register_backend("stub", kind="test double", requires="nothing", probe=lambda: True,
+                         factory=lambda top, par, **kw: Zero())
+    try:
+        assert "stub" in sto.available_backend_ids()
+        traj = integrate(Topology.decoupled(3), params,
+                         RunConfig(n=3, steps=20, dt=1e-11, backend="stub"))
+        assert np.array_equal(traj.states[-1], traj.states[0])
+    finally:
+        sto.unregister_backend("stub")
+    assert "stub" not in sto.available_backend_ids()
+
+
+def test_probe_that_raises_counts_as_unavailable(params):
+    def boom():
+        raise RuntimeError("probe exploded")
+
+    sto.register_backend("flaky", kind="t", requires="t", probe=boom, factory=lambda *a, **k: 0)
+    try:
+        assert "flaky" not in sto.available_backend_ids()
+        with pytest.raises(BackendUnavailableError):
+            sto.create_backend("flaky", Topology.decoupled(1), params)
+    finally:
+        sto.unregister_backend("flaky")
+
+
+# --------------------------------------------- derivative-only plugin path ----
+class _Stub:
+    def __init__(self, fn):
+        self.fn, self.calls, self.seen_u = fn, 0, []
+
+    def derivative(self, m, u, out):
+        self.calls += 1
+        self.seen_u.append(float(u[0]))
+        self.fn(m, u, out)
+        return out
+
+
+def test_plugin_zero_derivative_fixed_point(params):
+    stub = _Stub(lambda m, u, out: out.fill(0.0))
+    traj = integrate(Topology.decoupled(3), params, RunConfig(n=3, steps=50, dt=1e-11),
+                     backend=stub)
+    assert np.array_equal(traj.states[-1], traj.states[0])
+    assert stub.calls == 200 and traj.max_norm_drift == 0.0
+
+
+def test_plugin_zoh_held_across_stages(params):
+    series = InputSeries(samples=np.array([[10.0], [20.0]]), steps_per_sample=2)
+    stub = _Stub(lambda m, u, out: out.fill(0.0))
+    integrate(Topology.decoupled(1), params,
+              RunConfig(n=1, steps=4, dt=1e-11, input_series=series), backend=stub)
+    assert stub.seen_u == [10.0] * 8 + [20.0] * 8
+
+
+def test_rk4_step_is_degree4_taylor():
+    m = np.full((2, 3), 1.0)
+    rk4_step(lambda s, u, out: np.multiply(s, -2.0, out=out), m, np.zeros(1), 0.125,
+             RK4Scratch(2))
+    x = -0.25
+    assert np.abs(m - (1 + x + x**2 / 2 + x**3 / 6 + x**4 / 24)).max() <= 1e-16
+
+
+def test_plugin_divergence_location(params):
+    def poison(m, u, out):
+        out.fill(0.0)
+        out[2, 0] = np.inf
+
+    with pytest.raises(IntegrationDivergedError) as info:
+        integrate(Topology.decoupled(4), params, RunConfig(n=4, steps=5, dt=1e-11),
+                  backend=_Stub(poison))
+    assert (info.value.oscillator, info.value.step) == (2, 1)
+
+
+def test_validation_errors(params):
+    with pytest.raises(ParameterError):
+        integrate(Topology.decoupled(3), params, RunConfig(n=4, steps=1, dt=1e-11))
+    with pytest.raises(ParameterError):
+        integrate(Topology.decoupled(3), params,
+                  RunConfig(n=3, steps=1, dt=1e-11, input_series=InputSeries.zeros(2)))
+    with pytest.raises(ParameterError):
+        integrate(Topology.decoupled(1), params,
+                  RunConfig(n=1, steps=7, dt=1e-11,
+                            input_series=InputSeries(np.ones((3, 1)), 1)))
+
+
+def test_compare_trajectories_grid_checks(params):
+    stub = _Stub(lambda m, u, out: out.fill(0.0))
+    a = integrate(Topology.decoupled(2), params, RunConfig(n=2, steps=10, dt=1e-11), backend=stub)
+    b = integrate(Topology.decoupled(2), params, RunConfig(n=2, steps=11, dt=1e-11), backend=stub)
+    c = integrate(Topology.decoupled(2), params, RunConfig(n=2, steps=10, dt=2e-11), backend=stub)
+    assert compare_trajectories(a, a) == 0.0
+    for other in (b, c):
+        with pytest.raises(TrajectoryMismatchError):
+            compare_trajectories(a, other)
+
+
+def test_trajectory_csv_round_trip(tmp_path, params):
+    stub = _Stub(lambda m, u, out: np.multiply(m, -1e9, out=out))
+    traj = integrate(Topology.decoupled(2), params, RunConfig(n=2, steps=3, dt=1e-11),
+                     backend=stub)
+    path = tmp_path / "t.csv"
+    sto.write_trajectory_csv(path, traj)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "t,k,mx,my,mz" and len(lines) == 1 + traj.n_recorded * 2
+    t, k, mx, my, mz = lines[-1].split(",")
+    assert float(t) == traj.times[-1] and int(k) == 1
+    assert (float(mx), float(my), float(mz)) == tuple(traj.states[-1, 1])
