@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark: oscillator-steps/s of the coupled-STO RK4 path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+One bench "step" = one whole integrate() run of the workload (BASELINE.json
+configs): N oscillators x S RK4 steps, recorded initial + final
+(record_stride = S, as the reference's run_benchmark does, bench.py:291).
+Metric = N * S / seconds per run (oscillator-steps/s), summed over ranks.
+
+Default workload "n1e4" = configs[4] at N = 1e4 (the largest N of the
+metric's N=1..1e4 range that fits one GPU; W = 800 MB > L2, so no L2 flush
+is needed between runs). Other workloads: n1 (configs[1]), n100
+(configs[0]), n1000 (configs[2]), n4e4.
+
+Arms
+  ours (default)  value: device-resident inputs, CUDA events around K runs of
+                  sto_integrate (persistent kernel), max over ranks.
+                  e2e: the public API `integrate(topology, params, config)` from
+                  pinned host buffers: W/W_in/m0/drive uploaded, run, states read
+                  back -- every step.
+  reference       the reference's CPU path restated in C (oracle/, kind
+                  "port": the reference is pure Python/numba, nothing to
+                  compile) on all host cores, bounded sample of the workload.
+
+Multi-GPU (torchrun): ranks run independent replicas of the workload
+(the row-sharded single trajectory is not wired into bench yet), so
+scaling is "weak".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (n, rk4 steps per run, description, random drive)
+    "n1e4": (10_000, 1000, "configs[4]: N=1e4 coupled STOs, single trajectory, 1e3 RK4 steps", False),
+    "n4e4": (40_000, 50, "configs[4]: N=4e4 coupled STOs, single trajectory, 50 RK4 steps", False),
+    "n1000": (1000, 100_000, "configs[2]: N=1000, single trajectory, 1e5 RK4 steps", False),
+    "n100": (100, 10_000, "configs[0]: N=100, 1e4 RK4 steps, random drive", True),
+    "n1": (1, 1_000_000, "configs[1]: N=1 single STO, 1e6 RK4 steps", False),
+}
+DT = 1e-11
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def cached_topology(n: int, seed: int = 0):
+    """build_topology(n, seed) with a /dev/shm cache (same box, both arms)."""
+    import paper_2312_01121_b200 as sto
+
+    cache = Path("/dev/shm") / f"sto_topology_n{n}_s{seed}.npz"
+    if cache.exists():
+        try:
+            with np.load(cache) as z:
+                return sto.Topology(sto.CouplingMatrix(z["w"]), sto.InputWeights(z["w_in"]))
+        except Exception:
+            pass
+    top = sto.build_topology(n, n_in=1, seed=seed)
+    try:
+        tmp = cache.with_suffix(".tmp.npz")
+        np.savez(tmp, w=top.coupling.entries, w_in=top.input_weights.entries)
+        os.replace(tmp, cache)
+    except OSError:
+        pass
+    return top
+
+
+def drive_for(name: str, n_in: int = 1):
+    n, steps, _, random_drive = WORKLOADS[name]
+    if random_drive:
+        return np.random.default_rng(1).uniform(-1, 1, (steps, n_in)), 1
+    return np.zeros((1, n_in)), 1
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def oracle_sample(top, name: str, rk4_steps: int, threads: int):
+    """Time the CPU oracle (reference path restated in C) on `rk4_steps` steps."""
+    import paper_2312_01121_b200 as sto
+    from oracle import oracle
+
+    n = top.n
+    samples, sps = drive_for(name)
+    samples = samples[:max(1, min(samples.shape[0], rk4_steps))]
+    consts = sto.kernel_scalars(sto.PhysicalParams())
+    m0 = sto.initial_state(n)
+    t0 = time.perf_counter()
+    oracle.integrate(top.coupling.entries, top.input_weights.entries, consts, m0, samples, sps,
+                     DT, rk4_steps, rk4_steps, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_sample_steps(n: int) -> int:
+    """RK4 steps for a ~10-20 s oracle sample (about 1e10 osc-steps*N work)."""
+    return int(max(2, min(200_000, 4e10 / max(1.0, float(n) * n * 4) / 2)))
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    name = args.workload
+    n, steps, desc, _ = WORKLOADS[name]
+    top = cached_topology(n)
+    threads = os.cpu_count() or 1
+    sample = min(steps, cpu_sample_steps(n))
+    oracle_sample(top, name, min(sample, 2), threads)  # warm caches / page in W
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt = oracle_sample(top, name, sample, threads)
+        if i >= args.warmup:
+            times.append(dt)
+    sec = float(np.mean(times))
+    value = n * sample / sec
+    line = {
+        "impl": "reference", "metric": "oscillator-steps/s", "value": value,
+        "unit": "osc-steps/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (build_topology seed 0)",
+        "config": {"workload": desc, "n": n, "rk4_steps_per_sample": sample, "dt": DT,
+                   "parallelism": f"{threads} host threads (OpenMP, 128 fixed row blocks)"},
+        "cpu_baseline": {"value": value, "unit": "osc-steps/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"N={n}, {sample} RK4 steps per bench step (reference "
+                                   f"rk4_step/_row_derivative restated in C, oracle/)"},
+        "e2e": {"value": value, "unit": "osc-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_ncu_traffic(name: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(name)
+        except Exception:
+            return None
+    return None
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200 import _native
+    from paper_2312_01121_b200.backends.b200 import B200Backend
+
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+
+    name = args.workload
+    n, steps, desc, _ = WORKLOADS[name]
+    if args.rk4_steps:
+        steps = args.rk4_steps
+    stride = steps
+    params = sto.PhysicalParams()
+    if world > 1 and rank != 0:
+        dist.barrier()
+    top = cached_topology(n)
+    if world > 1 and rank == 0:
+        dist.barrier()
+    samples, sps = drive_for(name)
+    samples = samples[:steps] if samples.shape[0] > 1 else samples
+
+    # ------------------------------------------------------------ value ----
+    backend = B200Backend(top, params, device=dev)
+    info = backend.plan_info
+    nrec = _native.n_records(steps, stride)
+    m0 = torch.as_tensor(sto.initial_state(n), device="cuda")
+    samples_d = torch.as_tensor(samples, device="cuda")
+    m_d = torch.empty_like(m0)
+    states_d = torch.empty((nrec, n, 3), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def one_run():
+        m_d.copy_(m0)
+        backend._plan.integrate_dev(m_d, samples_d, sps, DT, steps, stride, states_d, sync=False)
+
+    for _ in range(args.warmup):
+        one_run()
+    backend._plan.last_status()
+    torch.cuda.synchronize()
+    kstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kstop = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clocks:
+        t_start.record(stream)
+        for i in range(args.steps):
+            m_d.copy_(m0)
+            kstart[i].record(stream)
+            backend._plan.integrate_dev(m_d, samples_d, sps, DT, steps, stride, states_d,
+                                        sync=False)
+            kstop[i].record(stream)
+        t_stop.record(stream)
+        torch.cuda.synchronize()
+    backend._plan.last_status()
+    total_s = t_start.elapsed_time(t_stop) / 1e3
+    kernel_s = float(np.mean([a.elapsed_time(b) for a, b in zip(kstart, kstop)])) / 1e3
+    if dist:
+        t = torch.tensor([total_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+    value = world * n * steps * args.steps / total_s
+    launches = 2 * args.steps  # reset_status_kernel + persistent RK4 kernel per run
+
+    # -------------------------------------------------------------- e2e ----
+    # pinned host copies of every input; public API call each step
+    w_pin = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    w_pin.numpy()[...] = top.coupling.entries
+    win_pin = torch.empty((n, 1), dtype=torch.float64, pin_memory=True)
+    win_pin.numpy()[...] = top.input_weights.entries
+    top_pinned = sto.Topology(sto.CouplingMatrix(w_pin.numpy()), sto.InputWeights(win_pin.numpy()))
+    series = sto.InputSeries(samples, sps)
+    cfg = sto.RunConfig(n=n, steps=steps, dt=DT, record_stride=stride, input_series=series,
+                        backend="gpu", gpu_device=dev)
+    e2e_steps = max(1, min(args.steps, 3))
+    sto.integrate(top_pinned, params, cfg)  # warm
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        traj = sto.integrate(top_pinned, params, cfg)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = 8 * (n * n + n * 1 + 3 * n + samples.size)
+    d2h = 8 * (traj.states.size + 3 * n)
+
+    # -------------------------------------------------------- roofline ----
+    peaks = measured_peaks()
+    alg_bytes = 32.0 * n * n * steps  # one f64 W row per RK stage per oscillator-step
+    achieved = alg_bytes / kernel_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                "traffic": load_ncu_traffic(name),
+                "peak_source": "fallback" if peaks.get("fallback") else "measured",
+                "kernel": f"grid_rk4_kernel[{info['kernel_name']}]"}
+
+    # ----------------------------------------------------- cpu baseline ----
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sample = min(steps, cpu_sample_steps(n))
+        oracle_sample(top, name, min(sample, 2), threads)
+        sec = oracle_sample(top, name, sample, threads)
+        cpu = {"value": n * sample / sec, "unit": "osc-steps/s", "cores": threads,
+               "kind": "port",
+               "sample": f"N={n}, {sample} RK4 steps (reference path restated in C, oracle/)"}
+
+    if rank == 0:
+        line = {
+            "metric": "oscillator-steps/s", "value": value, "unit": "osc-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_s * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (build_topology(n, seed=0), u=0 / seeded uniform drive)",
+            "config": {"workload": desc, "n": n, "rk4_steps_per_run": steps,
+                       "record_stride": stride, "dt": DT,
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "kernel": info["kernel_name"], "grid": info["grid"],
+                       "l2": ("inputs larger than L2 (W %.0f MB)" % (info["w_bytes"] / 1e6))
+                       if info["w_bytes"] > 126e6 else
+                       "W on-chip/L2-resident by design (persistent kernel; one launch per run)"},
+            "e2e": {"value": world * n * steps / e2e_s, "unit": "osc-steps/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="n1e4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rk4-steps", type=int, default=0, help="override RK4 steps per run")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local_rank = env_rank()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
 
     const long long total_stages = integrate ? 4 * p.steps : 1;
     const int nchunks = (cs.ldw + p.chunk_cols - 1) / p.chunk_cols;
-    const int blocks_per_chunk = p.chunk_cols / cs.blk;
+    // a single window covers every block even when ldw < blk (small n)
+    const int blocks_per_chunk = p.chunk_cols >= cs.ldw ? cs.nblocks : p.chunk_cols / cs.blk;
     const double *u = p.samples;
 
     for (long long e = 0; e < total_stages; ++e) {
