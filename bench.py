@@ -196,14 +196,15 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def load_ncu_traffic(name: str):
+def traffic_per_launch(name: str, rk4_steps: int):
+    """DRAM bytes (read + write) per persistent-kernel launch, from the committed
+    ncu capture (profiles/ncu_traffic.json, normalised per RK4 step)."""
     p = ROOT / "profiles" / "ncu_traffic.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text()).get(name)
-        except Exception:
-            return None
-    return None
+    try:
+        entry = json.loads(p.read_text()).get(name)
+        return float(entry["bytes_per_rk4_step"]) * rk4_steps if entry else None
+    except Exception:
+        return None
 
 
 def run_ours(args, rank, world, local_rank):
@@ -310,7 +311,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = alg_bytes / kernel_s / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                "traffic": load_ncu_traffic(name),
+                "traffic": traffic_per_launch(name, steps),
                 "peak_source": "fallback" if peaks.get("fallback") else "measured",
                 "kernel": f"grid_rk4_kernel[{info['kernel_name']}]"}
 

@@ -21,10 +21,10 @@ namespace sto {
 // ----------------------------------------------------------------------------
 // strict IEEE scalar helpers
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ double fmul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double fadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double fsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double fdiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a, b); }
 
 struct Consts {
     double c_prec, c_damp, h_appl, h_aniso, pref, lam, a_cp, a_in, px, py, pz;
@@ -37,50 +37,50 @@ struct V3 {
 // dm/dt of one oscillator given its coupling row sum `cp` and input row sum
 // `cin`.  cpu_jit.py:62-87 / model.py:239-301, operation for operation.
 __device__ __forceinline__ V3 row_rhs(V3 m, double cp, double cin, const Consts &c) {
-    double md = fadd(fmul(m.x, c.px), fmul(m.y, c.py));
-    md = fadd(md, fmul(m.z, c.pz));
-    const double hs = fdiv(c.pref, fadd(1.0, fmul(c.lam, md)));
+    double md = radd(rmul(m.x, c.px), rmul(m.y, c.py));
+    md = radd(md, rmul(m.z, c.pz));
+    const double hs = rdiv(c.pref, radd(1.0, rmul(c.lam, md)));
 
-    const double qx = fsub(fmul(c.py, m.z), fmul(c.pz, m.y));
-    const double qy = fsub(fmul(c.pz, m.x), fmul(c.px, m.z));
-    const double qz = fsub(fmul(c.px, m.y), fmul(c.py, m.x));
+    const double qx = rsub(rmul(c.py, m.z), rmul(c.pz, m.y));
+    const double qy = rsub(rmul(c.pz, m.x), rmul(c.px, m.z));
+    const double qz = rsub(rmul(c.px, m.y), rmul(c.py, m.x));
 
-    const double bx = fadd(fadd(fmul(c.a_cp, cp), fmul(c.a_in, cin)), fmul(hs, qx));
-    const double by = fmul(hs, qy);
-    const double bz = fadd(fadd(c.h_appl, fmul(c.h_aniso, m.z)), fmul(hs, qz));
+    const double bx = radd(radd(rmul(c.a_cp, cp), rmul(c.a_in, cin)), rmul(hs, qx));
+    const double by = rmul(hs, qy);
+    const double bz = radd(radd(c.h_appl, rmul(c.h_aniso, m.z)), rmul(hs, qz));
 
-    const double ax = fsub(fmul(m.y, bz), fmul(m.z, by));
-    const double ay = fsub(fmul(m.z, bx), fmul(m.x, bz));
-    const double az = fsub(fmul(m.x, by), fmul(m.y, bx));
+    const double ax = rsub(rmul(m.y, bz), rmul(m.z, by));
+    const double ay = rsub(rmul(m.z, bx), rmul(m.x, bz));
+    const double az = rsub(rmul(m.x, by), rmul(m.y, bx));
 
-    const double ex = fsub(fmul(m.y, az), fmul(m.z, ay));
-    const double ey = fsub(fmul(m.z, ax), fmul(m.x, az));
-    const double ez = fsub(fmul(m.x, ay), fmul(m.y, ax));
+    const double ex = rsub(rmul(m.y, az), rmul(m.z, ay));
+    const double ey = rsub(rmul(m.z, ax), rmul(m.x, az));
+    const double ez = rsub(rmul(m.x, ay), rmul(m.y, ax));
 
     V3 d;
-    d.x = fsub(-fmul(c.c_prec, ax), fmul(c.c_damp, ex));
-    d.y = fsub(-fmul(c.c_prec, ay), fmul(c.c_damp, ey));
-    d.z = fsub(-fmul(c.c_prec, az), fmul(c.c_damp, ez));
+    d.x = rsub(-rmul(c.c_prec, ax), rmul(c.c_damp, ex));
+    d.y = rsub(-rmul(c.c_prec, ay), rmul(c.c_damp, ey));
+    d.z = rsub(-rmul(c.c_prec, az), rmul(c.c_damp, ez));
     return d;
 }
 
 // s = m + k*h   (integrator.py:107-108, 110-111, 113-114)
 __device__ __forceinline__ V3 stage_point(V3 m, V3 k, double h) {
-    return V3{fadd(m.x, fmul(k.x, h)), fadd(m.y, fmul(k.y, h)), fadd(m.z, fmul(k.z, h))};
+    return V3{radd(m.x, rmul(k.x, h)), radd(m.y, rmul(k.y, h)), radd(m.z, rmul(k.z, h))};
 }
 
 // acc = k1 + k2*2   (integrator.py:117-118)
 __device__ __forceinline__ V3 acc_k2(V3 k1, V3 k2) {
-    return V3{fadd(k1.x, fmul(k2.x, 2.0)), fadd(k1.y, fmul(k2.y, 2.0)),
-              fadd(k1.z, fmul(k2.z, 2.0))};
+    return V3{radd(k1.x, rmul(k2.x, 2.0)), radd(k1.y, rmul(k2.y, 2.0)),
+              radd(k1.z, rmul(k2.z, 2.0))};
 }
 
 // m + ((acc + (k3*2 + k4)) * dt_6)   (integrator.py:119-121)
 __device__ __forceinline__ V3 rk4_final(V3 m, V3 acc, V3 k3, V3 k4, double dt6) {
     V3 r;
-    r.x = fadd(m.x, fmul(fadd(acc.x, fadd(fmul(k3.x, 2.0), k4.x)), dt6));
-    r.y = fadd(m.y, fmul(fadd(acc.y, fadd(fmul(k3.y, 2.0), k4.y)), dt6));
-    r.z = fadd(m.z, fmul(fadd(acc.z, fadd(fmul(k3.z, 2.0), k4.z)), dt6));
+    r.x = radd(m.x, rmul(radd(acc.x, radd(rmul(k3.x, 2.0), k4.x)), dt6));
+    r.y = radd(m.y, rmul(radd(acc.y, radd(rmul(k3.y, 2.0), k4.y)), dt6));
+    r.z = radd(m.z, rmul(radd(acc.z, radd(rmul(k3.z, 2.0), k4.z)), dt6));
     return r;
 }
 
@@ -96,10 +96,10 @@ __device__ __forceinline__ double tree_dot_stream(const double *a, const double 
     double stk[32];
     unsigned cnt = 0;
     for (int i = 0; i < w; ++i) {
-        double v = fmul(a[i], b[i]);
+        double v = rmul(a[i], b[i]);
         int lvl = 0;
         while (cnt & (1u << lvl)) {
-            v = fadd(stk[lvl], v);
+            v = radd(stk[lvl], v);
             ++lvl;
         }
         stk[lvl] = v;
@@ -109,7 +109,7 @@ __device__ __forceinline__ double tree_dot_stream(const double *a, const double 
     bool have = false;
     for (int lvl = 0; lvl < 32; ++lvl) {
         if (cnt & (1u << lvl)) {
-            acc = have ? fadd(stk[lvl], acc) : stk[lvl];
+            acc = have ? radd(stk[lvl], acc) : stk[lvl];
             have = true;
         }
     }
@@ -120,7 +120,7 @@ __device__ __forceinline__ double tree_dot_stream(const double *a, const double 
 __device__ __forceinline__ double tree_inplace(double *buf, int w) {
     while (w > 1) {
         const int half = w >> 1;
-        for (int j = 0; j < half; ++j) buf[j] = fadd(buf[2 * j], buf[2 * j + 1]);
+        for (int j = 0; j < half; ++j) buf[j] = radd(buf[2 * j], buf[2 * j + 1]);
         if (w & 1) {
             buf[half] = buf[w - 1];
             w = half + 1;
@@ -217,17 +217,17 @@ __device__ __forceinline__ double segment_node(const double *wseg, const double 
     for (int i = 0; i < C / 2; ++i) {
         const double2 w = load_w2<S>(wseg + ((i << 5) + lane) * 2);
         const double2 x = *reinterpret_cast<const double2 *>(xseg + ((i << 5) + lane) * 2);
-        p[2 * i] = fmul(w.x, x.x);
-        p[2 * i + 1] = fmul(w.y, x.y);
+        p[2 * i] = rmul(w.x, x.x);
+        p[2 * i + 1] = rmul(w.y, x.y);
     }
 #pragma unroll
     for (int w = C; w > 1; w >>= 1) {
 #pragma unroll
-        for (int j = 0; j < w / 2; ++j) p[j] = fadd(p[2 * j], p[2 * j + 1]);
+        for (int j = 0; j < w / 2; ++j) p[j] = radd(p[2 * j], p[2 * j + 1]);
     }
     double v = p[0];
 #pragma unroll
-    for (int mask = 1; mask < 32; mask <<= 1) v = fadd(v, __shfl_xor_sync(0xffffffffu, v, mask));
+    for (int mask = 1; mask < 32; mask <<= 1) v = radd(v, __shfl_xor_sync(0xffffffffu, v, mask));
     return v;
 }
 
@@ -271,7 +271,7 @@ __device__ __forceinline__ double block_node(const ColSched &cs, int b, const do
         for (int k = cs.ntail - 1; k >= 0; --k) {
             const int col = cs.tail_base[k];
             const double v = tail_segment_node<S>(cs.tail_c[k], wrow + col, xwin + (col - x_base), lane);
-            t = (k == cs.ntail - 1) ? v : fadd(v, t);
+            t = (k == cs.ntail - 1) ? v : radd(v, t);
         }
 #pragma unroll
         for (int j = 0; j < kMaxLeaves; ++j)
@@ -284,7 +284,7 @@ __device__ __forceinline__ double block_node(const ColSched &cs, int b, const do
 #pragma unroll
         for (int j = 0; j < (kMaxLeaves >> (lvl + 1)); ++j) {
             if (2 * j + 1 < width)
-                leaf[j] = fadd(leaf[2 * j], leaf[2 * j + 1]);
+                leaf[j] = radd(leaf[2 * j], leaf[2 * j + 1]);
             else if (2 * j < width)
                 leaf[j] = leaf[2 * j];
         }

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
             }
             if (stage == 0) {
                 rs.cin(r) = (p.n_in == 1)
-                                ? fmul(p.w_in[k], u[0])
+                                ? rmul(p.w_in[k], u[0])
                                 : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
             }
             const V3 mk = rs.get(kSlotM, r);
@@ -325,18 +325,18 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
     // coupling row sum at the current published x (pinned pairwise tree)
     auto coupling = [&](double xown) -> double {
         if constexpr (NMAX == 1) {
-            return fmul(w[0], xown);
+            return rmul(w[0], xown);
         } else {
             double t[NMAX];
 #pragma unroll
-            for (int j = 0; j < NMAX; ++j) t[j] = (j < n) ? fmul(w[j], xsh[j]) : 0.0;
+            for (int j = 0; j < NMAX; ++j) t[j] = (j < n) ? rmul(w[j], xsh[j]) : 0.0;
             int width = n;
 #pragma unroll
             for (int half = NMAX / 2; half >= 1; half >>= 1) {
 #pragma unroll
                 for (int j = 0; j < half; ++j) {
                     if (2 * j + 1 < width)
-                        t[j] = fadd(t[2 * j], t[2 * j + 1]);
+                        t[j] = radd(t[2 * j], t[2 * j + 1]);
                     else if (2 * j < width)
                         t[j] = t[2 * j];
                 }
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
         const double *u = p.samples + idx * p.n_in;
         double cin = 0.0;
         if (live)
-            cin = (p.n_in == 1) ? fmul(p.w_in[k], u[0])
+            cin = (p.n_in == 1) ? rmul(p.w_in[k], u[0])
                                 : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
         const V3 k1 = row_rhs(m, coupling(m.x), cin, c);
         V3 s = stage_point(m, k1, p.h2);
