@@ -78,6 +78,8 @@ typedef struct {
 #define STO_PLAN_FORCE_RESIDENT 0x2  /* W slice held in shared memory per CTA     */
 #define STO_PLAN_FORCE_SINGLE   0x4  /* one CTA, exchange through shared memory   */
 #define STO_PLAN_NO_TINY        0x8  /* do not use the one-warp kernel for n<=32  */
+#define STO_PLAN_FORCE_REG      0x10 /* W register-resident teams (n <= 1024)     */
+#define STO_PLAN_NO_REG         0x20 /* do not use the register-resident kernel    */
 
 typedef struct {
     double *m;               /* device (n,3): initial state in, final state out    */
@@ -98,7 +100,8 @@ typedef struct {
 } sto_status;
 
 typedef struct {
-    int32_t kernel;          /* 0 tiny, 1 single-CTA, 2 SMEM-resident grid, 3 streaming grid */
+    int32_t kernel;          /* 0 tiny, 1 single-CTA, 2 SMEM-resident grid, 3 streaming grid,
+                                4 register-resident teams */
     int32_t grid;            /* CTAs of the persistent kernel                        */
     int32_t threads;         /* threads per CTA                                      */
     int32_t smem_bytes;      /* dynamic shared memory per CTA                        */

@@ -22,8 +22,9 @@ LIB_PATH = Path(__file__).resolve().parent / "libsto_b200.so"
 STO_OK, STO_E_UNAVAILABLE, STO_E_PARAM, STO_E_DIVERGED, STO_E_CUDA, STO_E_NOMEM = range(6)
 
 # flags of sto_plan_desc (include/sto.h)
-FORCE_STREAM, FORCE_RESIDENT, FORCE_SINGLE, NO_TINY = 0x1, 0x2, 0x4, 0x8
-KERNEL_NAMES = {0: "tiny", 1: "single", 2: "resident", 3: "stream"}
+FORCE_STREAM, FORCE_RESIDENT, FORCE_SINGLE, NO_TINY, FORCE_REG, NO_REG = (
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20)
+KERNEL_NAMES = {0: "tiny", 1: "single", 2: "resident", 3: "stream", 4: "reg"}
 
 _c_double_p = ctypes.POINTER(ctypes.c_double)
 

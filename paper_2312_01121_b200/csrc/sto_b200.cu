@@ -5,11 +5,13 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
 #include "../../include/sto.h"
 #include "sto_kernels.cuh"
+#include "sto_reg_kernel.cuh"
 
 using namespace sto;
 
@@ -99,11 +101,15 @@ __global__ void permute_rows_kernel(const double *__restrict__ src, long long ld
     }
 }
 
-__global__ void reset_status_kernel(StatusDev *st, unsigned long long *bar) {
-    st->flag = 0;
-    st->oscillator = 0x7fffffffffffffffLL;
-    st->step = -1;
-    *bar = 0ull;
+constexpr int kMaxFlags = 1024;
+
+__global__ void reset_status_kernel(StatusDev *st, unsigned long long *bar, unsigned *flags) {
+    for (int i = threadIdx.x; i < kMaxFlags; i += blockDim.x) flags[i] = 0u;
+    if (threadIdx.x == 0) {
+        st->flag = 0;
+        st->key = 0x7fffffffffffffffLL;
+        *bar = 0ull;
+    }
 }
 
 struct Layout {
@@ -129,7 +135,7 @@ int upload_layout(Layout &L, int rows, int cols, const double *a, long long lda,
     return STO_OK;
 }
 
-enum KernelKind { kTiny = 0, kSingle = 1, kResident = 2, kStream = 3 };
+enum KernelKind { kTiny = 0, kSingle = 1, kResident = 2, kStream = 3, kReg = 4 };
 
 }  // namespace
 
@@ -143,6 +149,7 @@ struct sto_plan {
     double *w_in = nullptr;
     double *xbuf = nullptr;
     unsigned long long *bar = nullptr;
+    unsigned *flags = nullptr;
     StatusDev *status = nullptr;
     // integrate launch configuration
     int kind = kStream;
@@ -151,6 +158,8 @@ struct sto_plan {
     int rows_cap = 1;
     int chunk_cols = 0;
     size_t smem = 0;
+    int threads = 512;
+    int team = 0;  // kReg: threads per row
 };
 
 namespace {
@@ -181,6 +190,43 @@ int launch_grid(const KParams &p, int grid, size_t smem, bool cooperative, cudaS
         STO_CUDA(cudaGetLastError());
     }
     return STO_OK;
+}
+
+template <int T, int C, bool SINGLE>
+int launch_reg_t(const RegParams &rp, int grid, int threads, size_t smem, cudaStream_t stream) {
+    auto fn = reg_rk4_kernel<T, C, SINGLE>;
+    STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (SINGLE) {
+        fn<<<1, threads, smem, stream>>>(rp);
+        STO_CUDA(cudaGetLastError());
+    } else {
+        void *args[] = {(void *)&rp};
+        STO_CUDA(cudaLaunchCooperativeKernel((void *)fn, dim3(grid), dim3(threads), args, smem,
+                                             stream));
+    }
+    return STO_OK;
+}
+
+// (team T, columns per thread C): n <= 128 uses C = 32 in one CTA; larger n
+// uses C = 16 over the grid.  P = T * C is the padded row width.
+int launch_reg(const RegParams &rp, int team, int cols, bool single, int grid, int threads,
+               size_t smem, cudaStream_t s) {
+    if (single) {
+        switch (team) {
+            case 1: return launch_reg_t<1, 32, true>(rp, grid, threads, smem, s);
+            case 2: return launch_reg_t<2, 32, true>(rp, grid, threads, smem, s);
+            default: return launch_reg_t<4, 32, true>(rp, grid, threads, smem, s);
+        }
+    }
+    (void)cols;
+    switch (team) {
+        case 2: return launch_reg_t<2, 16, false>(rp, grid, threads, smem, s);
+        case 4: return launch_reg_t<4, 16, false>(rp, grid, threads, smem, s);
+        case 8: return launch_reg_t<8, 16, false>(rp, grid, threads, smem, s);
+        case 16: return launch_reg_t<16, 16, false>(rp, grid, threads, smem, s);
+        case 32: return launch_reg_t<32, 16, false>(rp, grid, threads, smem, s);
+        default: return launch_reg_t<64, 16, false>(rp, grid, threads, smem, s);
+    }
 }
 
 int launch_tiny(const KParams &p, int n, cudaStream_t stream) {
@@ -276,6 +322,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     if (cudaMalloc(&P->w_in, sizeof(double) * (size_t)n * d->n_in) != cudaSuccess ||
         cudaMalloc(&P->xbuf, sizeof(double) * 2 * (size_t)cs.ldw) != cudaSuccess ||
         cudaMalloc(&P->bar, 64) != cudaSuccess ||
+        cudaMalloc(&P->flags, sizeof(unsigned) * kMaxFlags) != cudaSuccess ||
         cudaMalloc(&P->status, sizeof(StatusDev)) != cudaSuccess)
         return bail(fail(STO_E_NOMEM, "device allocation failed"));
     if (cudaMemcpy2D(P->w_in, sizeof(double) * d->n_in, d->w_in, sizeof(double) * d->ld_in,
@@ -284,15 +331,39 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         return bail(fail(STO_E_CUDA, "W_in upload failed"));
 
     // ---- choose the integrate kernel ------------------------------------
-    const bool no_tiny = d->flags & STO_PLAN_NO_TINY;
+    const int fl = d->flags;
+    const int forced = fl & (STO_PLAN_FORCE_STREAM | STO_PLAN_FORCE_RESIDENT |
+                             STO_PLAN_FORCE_SINGLE | STO_PLAN_FORCE_REG);
     const size_t single_smem = grid_smem(n, cs, cs.ldw, true);
-    if (n <= 32 && !no_tiny && !(d->flags & (STO_PLAN_FORCE_STREAM | STO_PLAN_FORCE_RESIDENT |
-                                             STO_PLAN_FORCE_SINGLE))) {
+    int pw = 32;
+    while (pw < n) pw <<= 1;
+    if (n <= 32 && !(fl & STO_PLAN_NO_TINY) && !forced) {
         P->kind = kTiny;
         P->grid = 1;
-    } else if ((d->flags & STO_PLAN_FORCE_SINGLE) ||
-               (!(d->flags & (STO_PLAN_FORCE_STREAM | STO_PLAN_FORCE_RESIDENT)) && n <= 128 &&
-                single_smem <= kSmemBudget)) {
+        P->threads = 32;
+    } else if ((fl & STO_PLAN_FORCE_REG) || (!forced && !(fl & STO_PLAN_NO_REG) && n <= 1024)) {
+        if (n > 1024) return bail(fail(STO_E_PARAM, "register-resident kernel needs n <= 1024"));
+        P->kind = kReg;
+        const bool single = n <= 128;
+        const int cols = single ? 32 : 16;  // W columns per thread (registers)
+        const int team = std::max(single ? 1 : 2, pw / cols);
+        P->team = team;
+        int g = 1;
+        if (!single) {
+            // ~512 threads per CTA, at most one CTA per SM
+            g = (int)std::min<long long>(P->sm_count, ((long long)n * team + 511) / 512);
+            if (const char *e = getenv("STO_REG_GRID")) g = std::max(1, std::min(atoi(e), P->sm_count));
+            g = std::max(g, (n * team + 511) / 512);
+        }
+        P->grid = g;
+        P->rows_cap = (n + g - 1) / g;
+        P->threads = ((P->rows_cap * team + 31) / 32) * 32;
+        P->chunk_cols = single ? 1 : 0;  // marks SINGLE for the launcher
+        P->smem = sizeof(double) * ((size_t)team * cols + 15 * (size_t)(P->threads / team) + 8);
+        if (P->threads > 512 || g > kMaxFlags)
+            return bail(fail(STO_E_PARAM, "register-resident kernel does not fit"));
+    } else if ((fl & STO_PLAN_FORCE_SINGLE) ||
+               (!forced && n <= 128 && single_smem <= kSmemBudget)) {
         if (single_smem > kSmemBudget)
             return bail(fail(STO_E_PARAM, "single-CTA kernel does not fit shared memory"));
         P->kind = kSingle;
@@ -304,8 +375,8 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         int g = std::min(P->sm_count, n);
         P->rows_cap = (n + g - 1) / g;
         const size_t res_smem = grid_smem(P->rows_cap, cs, cs.ldw, true);
-        const bool want_res = (d->flags & STO_PLAN_FORCE_RESIDENT) ||
-                              (!(d->flags & STO_PLAN_FORCE_STREAM) && res_smem <= kSmemBudget);
+        const bool want_res = (fl & STO_PLAN_FORCE_RESIDENT) ||
+                              (!(fl & STO_PLAN_FORCE_STREAM) && res_smem <= kSmemBudget);
         if (want_res) {
             if (res_smem > kSmemBudget)
                 return bail(fail(STO_E_PARAM, "resident kernel does not fit shared memory"));
@@ -332,6 +403,7 @@ void sto_plan_destroy(sto_plan *P) {
     cudaFree(P->w_in);
     cudaFree(P->xbuf);
     cudaFree(P->bar);
+    cudaFree(P->flags);
     cudaFree(P->status);
     delete P;
 }
@@ -340,7 +412,7 @@ int sto_plan_get_info(const sto_plan *P, sto_plan_info *info) {
     if (!P || !info) return fail(STO_E_PARAM, "null plan or info");
     info->kernel = P->kind;
     info->grid = P->grid;
-    info->threads = P->kind == kTiny ? 32 : kThreads;
+    info->threads = (P->kind == kTiny || P->kind == kReg) ? P->threads : kThreads;
     info->smem_bytes = (int)P->smem;
     info->ldw = P->L.cs.ldw;
     info->block_cols = P->L.cs.blk;
@@ -389,11 +461,16 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
     p.states = r->states;
     p.rows_cap = P->rows_cap;
     p.chunk_cols = P->chunk_cols;
-    reset_status_kernel<<<1, 1, 0, s>>>(P->status, P->bar);
+    reset_status_kernel<<<1, 256, 0, s>>>(P->status, P->bar, P->flags);
     STO_CUDA(cudaGetLastError());
     int rc = STO_OK;
     switch (P->kind) {
         case kTiny: rc = launch_tiny(p, P->n, s); break;
+        case kReg: {
+            RegParams rp{p, P->flags, P->xbuf};
+            rc = launch_reg(rp, P->team, 0, P->chunk_cols == 1, P->grid, P->threads, P->smem, s);
+            break;
+        }
         case kSingle: rc = launch_grid<WSrc::Shared, true>(p, 1, P->smem, false, s); break;
         case kResident: rc = launch_grid<WSrc::Shared, false>(p, P->grid, P->smem, true, s); break;
         default:
@@ -415,12 +492,12 @@ int sto_plan_last_status(sto_plan *P, sto_status *status, void *stream) {
     STO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     status->diverged = h.flag;
     status->reserved = 0;
-    status->oscillator = h.flag ? h.oscillator : -1;
-    status->step = h.flag ? h.step : -1;
+    status->oscillator = h.flag ? (h.key & 0xffffff) : -1;
+    status->step = h.flag ? (h.key >> 24) : -1;
     if (h.flag)
         return fail(STO_E_DIVERGED, "non-finite state for oscillator " +
-                                        std::to_string(h.oscillator) + " at step " +
-                                        std::to_string(h.step));
+                                        std::to_string(status->oscillator) + " at step " +
+                                        std::to_string(status->step));
     return STO_OK;
 }
 

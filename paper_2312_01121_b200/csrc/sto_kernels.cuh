@@ -20,12 +20,19 @@
 
 namespace sto {
 
+// Divergence report: `key` = (step << 24) | oscillator, minimised atomically,
+// so the earliest recorded step wins and, within it, the first oscillator --
+// the reference's (argmax over rows of the first non-finite record, that
+// step) convention (integrator.py:174-177).
 struct StatusDev {
     int32_t flag;
     int32_t pad;
-    long long oscillator;
-    long long step;
+    long long key;
 };
+__device__ __forceinline__ void report_divergence(StatusDev *st, long long step, int k) {
+    atomicMin(&st->key, (step << 24) | (long long)k);
+    st->flag = 1;
+}
 
 enum KernelMode : int { kIntegrate = 0, kDerivative = 1, kMatvec = 2 };
 
@@ -251,9 +258,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
                 xpub = mn.x;
                 if (rec >= 0) {
                     if (!all_finite(mn)) {
-                        atomicMin(&p.status->oscillator, (long long)k);
-                        p.status->step = step;
-                        p.status->flag = 1;
+                        report_divergence(p.status, step, k);
                         *sflag = 1;
                     } else if (p.states) {
                         double *st = p.states + ((size_t)rec * p.rows + k) * 3;
@@ -354,13 +359,16 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
     };
     publish(m.x);
     int diverged = 0;
-    for (long long step = 1; step <= p.steps; ++step) {
-        const long long idx = p.n_samples == 1 ? 0 : (step - 1) / p.sps;
-        const double *u = p.samples + idx * p.n_in;
-        double cin = 0.0;
+    long long next_rec = p.stride, rec_idx = 1;
+    const double *u = p.samples;
+    double cin = 0.0;
+    auto input_field = [&]() {
         if (live)
             cin = (p.n_in == 1) ? rmul(p.w_in[k], u[0])
                                 : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
+    };
+    input_field();
+    for (long long step = 1; step <= p.steps; ++step) {
         const V3 k1 = row_rhs(m, coupling(m.x), cin, c);
         V3 s = stage_point(m, k1, p.h2);
         publish(s.x);
@@ -374,16 +382,12 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
         const V3 k4 = row_rhs(s, coupling(s.x), cin, c);
         m = rk4_final(m, acc, k3, k4, p.dt6);
         publish(m.x);
-        const long long rec = record_index(step, p.stride, p.steps, p.n_records);
-        if (rec >= 0) {
+        if (step == next_rec || step == p.steps) {
+            const long long rec = (step == next_rec) ? rec_idx : p.n_records - 1;
             const bool bad = live && !all_finite(m);
             const unsigned badmask = __ballot_sync(0xffffffffu, bad);
             if (badmask) {
-                if (k == 0) {
-                    p.status->oscillator = __ffs(badmask) - 1;
-                    p.status->step = step;
-                    p.status->flag = 1;
-                }
+                if (k == 0) report_divergence(p.status, step, __ffs(badmask) - 1);
                 diverged = 1;
                 break;
             }
@@ -393,6 +397,14 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
                 st[1] = m.y;
                 st[2] = m.z;
             }
+            if (step == next_rec) {
+                next_rec += p.stride;
+                ++rec_idx;
+            }
+        }
+        if (p.n_samples > 1) {
+            u = p.samples + (step / p.sps) * p.n_in;
+            input_field();
         }
     }
     if (live && !diverged) {
