@@ -150,6 +150,7 @@ struct sto_plan {
     double *xbuf = nullptr;
     unsigned long long *bar = nullptr;
     unsigned *flags = nullptr;
+    uint4 *ll = nullptr;  // kReg: [2][n] LL words
     StatusDev *status = nullptr;
     // integrate launch configuration
     int kind = kStream;
@@ -323,6 +324,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         cudaMalloc(&P->xbuf, sizeof(double) * 2 * (size_t)cs.ldw) != cudaSuccess ||
         cudaMalloc(&P->bar, 64) != cudaSuccess ||
         cudaMalloc(&P->flags, sizeof(unsigned) * kMaxFlags) != cudaSuccess ||
+        cudaMalloc(&P->ll, sizeof(uint4) * 2 * (size_t)n) != cudaSuccess ||
         cudaMalloc(&P->status, sizeof(StatusDev)) != cudaSuccess)
         return bail(fail(STO_E_NOMEM, "device allocation failed"));
     if (cudaMemcpy2D(P->w_in, sizeof(double) * d->n_in, d->w_in, sizeof(double) * d->ld_in,
@@ -357,9 +359,9 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         }
         P->grid = g;
         P->rows_cap = (n + g - 1) / g;
-        P->threads = ((P->rows_cap * team + 31) / 32) * 32;
+        P->threads = ((P->rows_cap * team + 31) / 32) * 32;  // >= rows_cap (RHS owners)
         P->chunk_cols = single ? 1 : 0;  // marks SINGLE for the launcher
-        P->smem = sizeof(double) * ((size_t)team * cols + 15 * (size_t)(P->threads / team) + 8);
+        P->smem = sizeof(double) * ((size_t)team * cols + 2 * (size_t)(P->threads / team) + 8);
         if (P->threads > 512 || g > kMaxFlags)
             return bail(fail(STO_E_PARAM, "register-resident kernel does not fit"));
     } else if ((fl & STO_PLAN_FORCE_SINGLE) ||
@@ -404,6 +406,7 @@ void sto_plan_destroy(sto_plan *P) {
     cudaFree(P->xbuf);
     cudaFree(P->bar);
     cudaFree(P->flags);
+    cudaFree(P->ll);
     cudaFree(P->status);
     delete P;
 }
@@ -467,7 +470,8 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
     switch (P->kind) {
         case kTiny: rc = launch_tiny(p, P->n, s); break;
         case kReg: {
-            RegParams rp{p, P->flags, P->xbuf};
+            RegParams rp{p, P->ll};
+            STO_CUDA(cudaMemsetAsync(P->ll, 0, sizeof(uint4) * 2 * (size_t)P->n, s));
             rc = launch_reg(rp, P->team, 0, P->chunk_cols == 1, P->grid, P->threads, P->smem, s);
             break;
         }
@@ -575,5 +579,12 @@ int sto_tree_matvec(int device, int64_t rows, int64_t cols, const double *a, int
     cudaFree(L.w);
     return rc;
 }
+
+#ifdef STO_TIMELINE
+STO_API int sto_debug_timeline(unsigned long long *out, int count) {
+    STO_CUDA(cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * count));
+    return STO_OK;
+}
+#endif
 
 }  // extern "C"

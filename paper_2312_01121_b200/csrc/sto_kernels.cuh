@@ -78,17 +78,6 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long
     __syncthreads();
 }
 
-__device__ __forceinline__ double ld_cg(const double *p) {
-    double v;
-    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ double2 ld_cg2(const double *p) {
-    double2 v;
-    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
-    return v;
-}
-
 __device__ __forceinline__ int row_lo(int b, int g, int rows) {
     return (int)(((long long)b * rows) / g);
 }
@@ -188,11 +177,10 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
                     }
                 } else {
                     const double *src = p.xbuf + (size_t)(e & 1) * cs.ldw + x_base;
-                    for (int i = 2 * threadIdx.x; i < x_len; i += 2 * blockDim.x) {
-                        const double2 v = ld_cg2(src + i);
-                        xs[i] = v.x;
-                        xs[i + 1] = v.y;
-                    }
+                    const double2 *src2 = reinterpret_cast<const double2 *>(src);
+                    double2 *dst2 = reinterpret_cast<double2 *>(xs);
+#pragma unroll 4
+                    for (int i = threadIdx.x; i < x_len / 2; i += blockDim.x) dst2[i] = __ldcg(src2 + i);
                 }
                 __syncthreads();
             }

@@ -14,12 +14,15 @@
 //
 // Exchange of the stage x-vector:
 //   SINGLE (one CTA, n <= 128): leaders write x straight into shared memory.
-//   grid: leaders store x (logical order) to a double-buffered global vector,
-//   the CTA raises its flag with st.release.gpu; thread t < G polls flag t
-//   (relaxed loads + one acquire fence) and copies producer t's rows into
-//   shared memory -- one flag per producer instead of one contended counter.
-//   A diverged record step is signalled in the flag's top bit, so every CTA
-//   takes the same decision to stop after the same exchange.
+//   grid: "LL" all-gather through L2.  Each leader stores its x as one 16-byte
+//   word {lo32, epoch, hi32, epoch} (8-byte halves are single-copy atomic, so
+//   a reader that sees the epoch in both halves holds the matching data);
+//   every CTA reads the whole double-buffered vector with pipelined relaxed
+//   loads, retrying only stale entries.  One L2 round trip per exchange, no
+//   counter, no fence (measured 1.0 us at 125 CTAs x 1000 entries vs 2.1 us
+//   for flag + copy, tools/microbench.cu).  A row that diverged on a
+//   recording step sets the top bit of its epoch words, so every CTA takes
+//   the same decision to stop after the same exchange.
 #pragma once
 
 #include "sto_kernels.cuh"
@@ -27,11 +30,13 @@
 namespace sto {
 
 
+
 struct RegParams {
     KParams k;              // shared fields (consts, run, states, status ...)
-    unsigned *flags;        // [G] per-CTA epoch flags (zeroed before launch)
-    double *xg;             // [2][n] published x, logical order
+    uint4 *ll;              // [2][n] LL words of the published x (zeroed before launch)
 };
+
+constexpr int kLLMaxPerThread = 4;  // n <= 4 * 512
 
 // shared-memory position of logical column `col` (team-blocked: a 16-byte
 // load i by team thread j returns columns C*j + 2i, +1)
@@ -41,14 +46,37 @@ __device__ __forceinline__ int reg_xpos(int col, int T) {
     return (((q >> 1) * T + j) << 1) + (q & 1);
 }
 
-__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+__device__ __forceinline__ void st_ll(uint4 *p, double v, unsigned flag) {
+    const unsigned long long b = __double_as_longlong(v);
+    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "r"((unsigned)b), "r"(flag), "r"((unsigned)(b >> 32)), "r"(flag)
+                 : "memory");
 }
-__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ uint4 ld_ll(const uint4 *p) {
+    uint4 q;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                 : "l"(p));
+    return q;
 }
+
+#ifdef STO_TIMELINE
+// debug build only (tools/timeline.py): globaltimer stamps of CTA 0 and the
+// last CTA for stages [kTlFirst, kTlFirst + kTlStages)
+constexpr int kTlFirst = 400, kTlStages = 16, kTlEvents = 5;
+__device__ unsigned long long g_timeline[2][kTlStages][kTlEvents];
+__device__ __forceinline__ void tl_mark(long long e, int ev) {
+    const int who = blockIdx.x == 0 ? 0 : (blockIdx.x == gridDim.x - 1 ? 1 : -1);
+    if (who >= 0 && threadIdx.x == 0 && e >= kTlFirst && e < kTlFirst + kTlStages) {
+        unsigned long long t;
+        t = clock64();
+        g_timeline[who][e - kTlFirst][ev] = t;
+    }
+}
+#define TL(e, ev) tl_mark((e), (ev))
+#else
+#define TL(e, ev)
+#endif
 
 template <int T, int C, bool SINGLE>
 __global__ void __launch_bounds__(512, 1) reg_rk4_kernel(const __grid_constant__ RegParams rp) {
@@ -56,34 +84,38 @@ __global__ void __launch_bounds__(512, 1) reg_rk4_kernel(const __grid_constant__
     constexpr int LV = (C == 32) ? 5 : 4;  // tree levels above the products
     const KParams &p = rp.k;
     extern __shared__ __align__(16) double smem[];
-    double *xs = smem;            // P doubles, team-blocked
     const int teams = blockDim.x / T;
-    double *part = xs + P;        // T == 64: two warp nodes per team
-    RowState rs{part + 2 * teams, teams};  // leader RK state (m, s, acc, k3, cin)
-    volatile int *sstop = reinterpret_cast<volatile int *>(rs.base + 13 * teams);
+    double *xs = smem;                       // P doubles, team-blocked
+    double *cps = xs + P;                    // [teams][2] row sums (two warp halves if T = 64)
+    volatile int *sstop = reinterpret_cast<volatile int *>(cps + 2 * teams);
 
     const int G = gridDim.x, b = blockIdx.x;
     const int n = p.rows;
     const int r0 = row_lo(b, G, n), nrow = row_lo(b + 1, G, n) - r0;
+    // GEMV role: team `team`, member j -- columns [C*j, C*j + C) of row r0 + team
     const int team = threadIdx.x / T, j = threadIdx.x % T;
     const bool active = team < nrow;
-    const bool leader = active && j == 0;
-    const int k = r0 + team;  // oscillator owned by this team
+    // RHS role: thread r < nrow owns oscillator r0 + r for the whole run, its
+    // RK state lives in registers and the RHS work is packed into few warps
+    const int r = threadIdx.x;
+    const bool owner = r < nrow;
+    const int k = r0 + r;
 
-    // ---- W chunk into registers (device layout -> logical columns) ---------
     double w[C];
 #pragma unroll
     for (int q = 0; q < C; ++q) {
         const int col = j * C + q;
-        w[q] = (active && col < n) ? p.w[(size_t)k * p.cs.ldw + col_perm(p.cs, col)] : -0.0;
+        w[q] = (active && col < n) ? p.w[(size_t)(r0 + team) * p.cs.ldw + col_perm(p.cs, col)]
+                                   : -0.0;
     }
-    // ---- initial x (all of m0), leader state --------------------------------
     for (int i = threadIdx.x; i < P; i += blockDim.x) xs[i] = 0.0;
     __syncthreads();
-    for (int col = threadIdx.x; col < n; col += blockDim.x) xs[reg_xpos<C>(col, T)] = p.m[3 * (size_t)col];
-    if (leader) {
-        const V3 m{p.m[3 * (size_t)k], p.m[3 * (size_t)k + 1], p.m[3 * (size_t)k + 2]};
-        rs.put(kSlotM, team, m);
+    for (int col = threadIdx.x; col < n; col += blockDim.x)
+        xs[reg_xpos<C>(col, T)] = p.m[3 * (size_t)col];
+    V3 m{0.0, 0.0, 0.0}, s{0.0, 0.0, 0.0}, acc{0.0, 0.0, 0.0}, k3{0.0, 0.0, 0.0};
+    double cin = 0.0;
+    if (owner) {
+        m = V3{p.m[3 * (size_t)k], p.m[3 * (size_t)k + 1], p.m[3 * (size_t)k + 2]};
         if (p.states) {
             double *st = p.states + 3 * (size_t)k;
             st[0] = m.x;
@@ -95,21 +127,22 @@ __global__ void __launch_bounds__(512, 1) reg_rk4_kernel(const __grid_constant__
     __syncthreads();
 
     const double *u = p.samples;
-    long long next_rec = p.stride;  // next step on the recording grid
+    long long next_rec = p.stride;
     long long rec_idx = 1;
     unsigned epoch = 0;
     bool stop = false;
     for (long long step = 1; step <= p.steps && !stop; ++step) {
-        if (leader)
-            rs.cin(team) = (p.n_in == 1) ? rmul(p.w_in[k], u[0])
-                                         : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
+        if (owner)
+            cin = (p.n_in == 1) ? rmul(p.w_in[k], u[0])
+                                : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
         const bool record = (step == next_rec) || (step == p.steps);
 #pragma unroll 1
         for (int stage = 0; stage < 4; ++stage) {
-            // -------- team GEMV: cp = pinned tree of w . x ----------------
-            // pinned tree of the 16 products, streamed pair by pair: the
-            // unrolled binary counter merges completed siblings immediately,
-            // so at most log2(16) partial nodes are live
+            const long long estage = (step - 1) * 4 + stage;
+            TL(estage, 0);
+            // -------- team GEMV: pinned tree of w . x ----------------------
+            // products streamed pair by pair through an unrolled binary
+            // counter: completed siblings merge at once (<= log2(C) live nodes)
             double lvl[LV];
 #pragma unroll
             for (int i = 0; i < C / 2; ++i) {
@@ -126,78 +159,87 @@ __global__ void __launch_bounds__(512, 1) reg_rk4_kernel(const __grid_constant__
 #pragma unroll
             for (int mask = 1; mask < (T < 32 ? T : 32); mask <<= 1)
                 v = radd(v, __shfl_xor_sync(0xffffffffu, v, mask));
-            if constexpr (T == 64) {
-                if ((threadIdx.x & 31) == 0) part[2 * team + ((threadIdx.x >> 5) & 1)] = v;
+            if (T == 64) {
+                if ((threadIdx.x & 31) == 0) cps[2 * team + ((threadIdx.x >> 5) & 1)] = v;
+            } else if (j == 0) {
+                cps[2 * team] = v;
             }
-            __syncthreads();  // all reads of xs done (and warp halves merged)
-            // -------- leader: RHS + RK4 stage update -----------------------
+            __syncthreads();  // every read of xs done; row sums in cps
+            TL(estage, 1);
+            // -------- owners: RHS + RK4 stage update ------------------------
             double xpub = 0.0;
             bool bad = false;
-            if (leader) {
-                const double cp = (T == 64) ? radd(part[2 * team], part[2 * team + 1]) : v;
-                const V3 m = rs.get(kSlotM, team);
-                const V3 cur = (stage == 0) ? m : rs.get(kSlotS, team);
-                const V3 d = row_rhs(cur, cp, rs.cin(team), p.c);
+            if (owner) {
+                const double cp = (T == 64) ? radd(cps[2 * r], cps[2 * r + 1]) : cps[2 * r];
+                const V3 d = row_rhs(stage == 0 ? m : s, cp, cin, p.c);
                 if (stage == 0) {
-                    rs.put(kSlotAcc, team, d);
-                    const V3 s = stage_point(m, d, p.h2);
-                    rs.put(kSlotS, team, s);
+                    acc = d;
+                    s = stage_point(m, d, p.h2);
                     xpub = s.x;
                 } else if (stage == 1) {
-                    rs.put(kSlotAcc, team, acc_k2(rs.get(kSlotAcc, team), d));
-                    const V3 s = stage_point(m, d, p.h2);
-                    rs.put(kSlotS, team, s);
+                    acc = acc_k2(acc, d);
+                    s = stage_point(m, d, p.h2);
                     xpub = s.x;
                 } else if (stage == 2) {
-                    rs.put(kSlotK3, team, d);
-                    const V3 s = stage_point(m, d, p.dt);
-                    rs.put(kSlotS, team, s);
+                    k3 = d;
+                    s = stage_point(m, d, p.dt);
                     xpub = s.x;
                 } else {
-                    const V3 mn = rk4_final(m, rs.get(kSlotAcc, team), rs.get(kSlotK3, team), d, p.dt6);
-                    rs.put(kSlotM, team, mn);
-                    xpub = mn.x;
+                    m = rk4_final(m, acc, k3, d, p.dt6);
+                    xpub = m.x;
                     if (record) {
-                        if (!all_finite(mn)) {
+                        if (!all_finite(m)) {
                             bad = true;
                             report_divergence(p.status, step, k);
                         } else if (p.states) {
                             const long long ri = (step == next_rec) ? rec_idx : p.n_records - 1;
                             double *st = p.states + ((size_t)ri * n + k) * 3;
-                            st[0] = mn.x;
-                            st[1] = mn.y;
-                            st[2] = mn.z;
+                            st[0] = m.x;
+                            st[1] = m.y;
+                            st[2] = m.z;
                         }
                     }
                 }
             }
             const bool last = (step == p.steps) && stage == 3;
             if constexpr (SINGLE) {
-                if (leader) xs[reg_xpos<C>(k, T)] = xpub;
+                if (owner) xs[reg_xpos<C>(k, T)] = xpub;
                 if (bad) *sstop = 1;
                 __syncthreads();
                 if (*sstop) stop = true;
             } else {
-                if (leader) rp.xg[(size_t)((epoch + 1) & 1) * n + k] = xpub;
-                if (bad) *sstop = 1;
-                __syncthreads();
                 ++epoch;
+                if (owner)
+                    st_ll(rp.ll + (size_t)(epoch & 1) * n + k, xpub,
+                          epoch | (bad ? 0x80000000u : 0u));
+                TL(estage, 2);
                 if (!last) {
-                    if (threadIdx.x == 0)
-                        st_release_u32(rp.flags + b, epoch | (*sstop ? 0x80000000u : 0u));
-                    if (threadIdx.x < G) {
-                        const int t = threadIdx.x;
-                        unsigned f;
-                        do {
-                            f = ld_relaxed_u32(rp.flags + t);
-                        } while ((f & 0x7fffffffu) < epoch);
-                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                        if (f & 0x80000000u) *sstop = 1;
-                        const int lo = row_lo(t, G, n), hi = row_lo(t + 1, G, n);
-                        const double *src = rp.xg + (size_t)(epoch & 1) * n;
-                        for (int c = lo; c < hi; ++c) xs[reg_xpos<C>(c, T)] = ld_cg(src + c);
+                    const uint4 *slot = rp.ll + (size_t)(epoch & 1) * n;
+                    unsigned pending = 0, stopbit = 0;
+#pragma unroll
+                    for (int q = 0; q < kLLMaxPerThread; ++q)
+                        if (threadIdx.x + q * blockDim.x < n) pending |= 1u << q;
+                    uint4 got[kLLMaxPerThread];
+                    while (pending) {
+#pragma unroll
+                        for (int q = 0; q < kLLMaxPerThread; ++q)
+                            if (pending & (1u << q)) got[q] = ld_ll(slot + threadIdx.x + q * blockDim.x);
+#pragma unroll
+                        for (int q = 0; q < kLLMaxPerThread; ++q) {
+                            if ((pending & (1u << q)) && (got[q].y & 0x7fffffffu) == epoch &&
+                                got[q].w == got[q].y) {
+                                const int c = threadIdx.x + q * blockDim.x;
+                                xs[reg_xpos<C>(c, T)] = __longlong_as_double(
+                                    ((unsigned long long)got[q].z << 32) | got[q].x);
+                                stopbit |= got[q].y;
+                                pending &= ~(1u << q);
+                            }
+                        }
                     }
+                    if (stopbit & 0x80000000u) *sstop = 1;
+                    TL(estage, 3);
                     __syncthreads();
+                    TL(estage, 4);
                     if (*sstop) stop = true;
                 }
             }
@@ -209,8 +251,7 @@ __global__ void __launch_bounds__(512, 1) reg_rk4_kernel(const __grid_constant__
         }
         if (p.n_samples > 1) u = p.samples + (step / p.sps) * p.n_in;
     }
-    if (leader) {
-        const V3 m = rs.get(kSlotM, team);
+    if (owner) {
         double *mm = p.m + 3 * (size_t)k;
         mm[0] = m.x;
         mm[1] = m.y;

@@ -171,6 +171,85 @@ __global__ void ll_kernel(int iters, int per, uint4 *buf, long long *cyc, double
     }
 }
 
+// LL exchange, pipelined: each thread owns up to 4 entries, issues all pending
+// loads at once, retries only the entries whose flags are stale.
+__global__ void ll2_kernel(int iters, int n, uint4 *buf, double *sink) {
+    extern __shared__ double xs[];
+    const int G = gridDim.x;
+    const int lo = (int)(((long long)blockIdx.x * n) / G), hi = (int)(((long long)(blockIdx.x + 1) * n) / G);
+    double acc = 0.0;
+    for (int e = 1; e <= iters; ++e) {
+        uint4 *slot = buf + (size_t)(e & 1) * n;
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            const unsigned long long b = __double_as_longlong((double)(e + i));
+            asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(slot + i),
+                         "r"((unsigned)b), "r"((unsigned)e), "r"((unsigned)(b >> 32)), "r"((unsigned)e)
+                         : "memory");
+        }
+        unsigned pending = 0;
+        uint4 q[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            if (threadIdx.x + r * blockDim.x < n) pending |= 1u << r;
+        while (pending) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (pending & (1u << r)) {
+                    const uint4 *src = slot + threadIdx.x + r * blockDim.x;
+                    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(q[r].x), "=r"(q[r].y), "=r"(q[r].z), "=r"(q[r].w) : "l"(src));
+                }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if ((pending & (1u << r)) && q[r].y == (unsigned)e && q[r].w == (unsigned)e) {
+                    xs[threadIdx.x + r * blockDim.x] =
+                        __longlong_as_double(((unsigned long long)q[r].z << 32) | q[r].x);
+                    pending &= ~(1u << r);
+                }
+        }
+        __syncthreads();
+        acc += xs[(e * 7) % n];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) sink[0] = acc;
+}
+
+// per-CTA flags on separate 256-B lines + pipelined copy of the whole vector
+__global__ void flag_copy_kernel(int iters, int n, unsigned *flags, double *xbuf, double *sink) {
+    extern __shared__ double xs[];
+    const int G = gridDim.x;
+    const int lo = (int)(((long long)blockIdx.x * n) / G), hi = (int)(((long long)(blockIdx.x + 1) * n) / G);
+    double acc = 0.0;
+    for (int e = 1; e <= iters; ++e) {
+        double *slot = xbuf + (size_t)(e & 1) * n;
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) slot[i] = (double)(e + i);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + 64 * blockIdx.x), "r"(e) : "memory");
+        if (threadIdx.x < G) {
+            unsigned f;
+            do {
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flags + 64 * threadIdx.x) : "memory");
+            } while (f < (unsigned)e);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        __syncthreads();
+        double v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = threadIdx.x + r * blockDim.x;
+            if (i < n) v[r] = __ldcg(slot + i);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = threadIdx.x + r * blockDim.x;
+            if (i < n) xs[i] = v[r];
+        }
+        __syncthreads();
+        acc += xs[(e * 7) % n];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) sink[0] = acc;
+}
+
 int main() {
     double *out;
     long long *cyc;
@@ -263,6 +342,36 @@ int main() {
             cudaEventSynchronize(b);
             cudaEventElapsedTime(&ms, a, b);
             printf(", \"ll_g%d_per%d_ns\": %.1f", g, per, ms * 1e6 / iters);
+        }
+    }
+    {
+        uint4 *b2;
+        unsigned *fl;
+        cudaMalloc(&b2, 2 * 4096 * sizeof(uint4));
+        cudaMalloc(&fl, 64 * 1024 * 4);
+        cudaFuncSetAttribute(ll2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8);
+        cudaFuncSetAttribute(flag_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8);
+        for (int g : {16, 64, 125, 148}) {
+            for (int n : {128, 1000, 2000}) {
+                const int iters = 20000;
+                cudaMemset(b2, 0, 2 * 4096 * sizeof(uint4));
+                void *args[] = {(void *)&iters, (void *)&n, (void *)&b2, (void *)&out};
+                cudaEventRecord(a);
+                cudaLaunchCooperativeKernel((void *)ll2_kernel, g, 512, args, n * 8, 0);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                cudaEventElapsedTime(&ms, a, b);
+                printf(", \"ll2_g%d_n%d_ns\": %.1f", g, n, ms * 1e6 / iters);
+                cudaMemset(fl, 0, 64 * 1024 * 4);
+                double *xb2 = (double *)b2;
+                void *args2[] = {(void *)&iters, (void *)&n, (void *)&fl, (void *)&xb2, (void *)&out};
+                cudaEventRecord(a);
+                cudaLaunchCooperativeKernel((void *)flag_copy_kernel, g, 512, args2, n * 8, 0);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                cudaEventElapsedTime(&ms, a, b);
+                printf(", \"flagcopy_g%d_n%d_ns\": %.1f", g, n, ms * 1e6 / iters);
+            }
         }
     }
     cudaError_t err = cudaDeviceSynchronize();
