@@ -51,7 +51,13 @@ WORKLOADS = {
     "n1000": (1000, 100_000, "configs[2]: N=1000, single trajectory, 1e5 RK4 steps", False),
     "n100": (100, 10_000, "configs[0]: N=100, 1e4 RK4 steps, random drive", True),
     "n1": (1, 1_000_000, "configs[1]: N=1 single STO, 1e6 RK4 steps", False),
+    "ens512": (1000, 10_000, "configs[3]: N=1000 x B=512 ensemble (current sweep 2.0-3.0 mA), "
+               "1e4 RK4 steps, FP64 tensor-core (DMMA) coupling GEMM", False),
 }
+ENSEMBLE_BATCH = {"ens512": 512}
+# FP64 peaks measured on this pool's B200 (tools/fp64_peak.cu; MEASURED_PEAKS.json has
+# none): DMMA m8n8k4 37.1 TFLOP/s, DFMA 34.0, cuBLAS DGEMM 8192^3 35.5.
+FP64_TENSOR_PEAK_TFLOPS = 37.1
 DT = 1e-11
 
 
@@ -90,6 +96,8 @@ def cached_topology(n: int, seed: int = 0):
 
 def drive_for(name: str, n_in: int = 1):
     n, steps, _, random_drive = WORKLOADS[name]
+    if name in ENSEMBLE_BATCH:
+        return np.zeros((1, n_in)), 1
     if random_drive:
         return np.random.default_rng(1).uniform(-1, 1, (steps, n_in)), 1
     return np.zeros((1, n_in)), 1
@@ -205,6 +213,121 @@ def traffic_per_launch(name: str, rk4_steps: int):
         return float(entry["bytes_per_rk4_step"]) * rk4_steps if entry else None
     except Exception:
         return None
+
+
+def run_ours_ensemble(args, rank, world, local_rank):
+    """configs[3]: B members sharing W, batch-sharded over ranks (no communication)."""
+    import torch
+
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200.backends.b200 import B200Backend
+
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    name = args.workload
+    n, steps, desc, _ = WORKLOADS[name]
+    if args.rk4_steps:
+        steps = args.rk4_steps
+    batch_total = ENSEMBLE_BATCH[name]
+    currents = np.linspace(2.0e-3, 3.0e-3, batch_total)
+    mine = np.array_split(np.arange(batch_total), world)[rank]   # batch sharding
+    params = [sto.PhysicalParams(current=float(c)) for c in currents[mine]]
+    top = cached_topology(n)
+    backend = B200Backend(top, params[0], device=dev)
+    consts = np.array([sto.kernel_scalars(p) for p in params])
+    batch = len(params)
+    stride = steps
+    from paper_2312_01121_b200 import _native
+
+    nrec = _native.n_records(steps, stride)
+    c_d = torch.as_tensor(consts, device="cuda")
+    m0 = torch.as_tensor(np.tile(sto.initial_state(n)[None], (batch, 1, 1)), device="cuda")
+    m_d = torch.empty_like(m0)
+    s_d = torch.zeros((1, 1), dtype=torch.float64, device="cuda")
+    states_d = torch.empty((nrec, batch, n, 3), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def one_run():
+        m_d.copy_(m0)
+        backend._plan.integrate_ensemble_dev(m_d, c_d, s_d, 1, 0, DT, steps, stride, states_d)
+
+    for _ in range(args.warmup):
+        one_run()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        t0e.record(stream)
+        for _ in range(args.steps):
+            one_run()
+        t1e.record(stream)
+        torch.cuda.synchronize()
+    total_s = t0e.elapsed_time(t1e) / 1e3
+    if dist:
+        t = torch.tensor([total_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+    value = batch_total * n * steps * args.steps / total_s
+    kernel_s = total_s / args.steps
+    flops = 8.0 * n * n * batch * steps  # 4 stages x 2N MACs per oscillator-step
+    achieved = flops / kernel_s / 1e12
+
+    # e2e through the public API, host buffers, each step
+    cfg = sto.RunConfig(n=n, steps=steps, dt=DT, record_stride=stride, gpu_device=dev)
+    sto.integrate_ensemble(top, params, cfg, backend=backend)
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 2))
+    for _ in range(e2e_steps):
+        ens = sto.integrate_ensemble(top, params, cfg, backend=backend)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sample = min(steps, cpu_sample_steps(n))
+        oracle_sample(top, "n1000", min(sample, 2), threads)
+        sec = oracle_sample(top, "n1000", sample, threads)
+        cpu = {"value": n * sample / sec, "unit": "osc-steps/s", "cores": threads, "kind": "port",
+               "sample": f"1 member of {batch_total}, N={n}, {sample} RK4 steps (members run "
+                         f"sequentially on the CPU, so the ensemble rate equals this rate)"}
+    if rank == 0:
+        line = {
+            "metric": "oscillator-steps/s", "value": value, "unit": "osc-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_s * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (build_topology(1000, seed=0), u=0, current sweep)",
+            "config": {"workload": desc, "n": n, "batch": batch_total, "rk4_steps_per_run": steps,
+                       "record_stride": stride, "dt": DT,
+                       "parallelism": f"batch-sharded x{world}" if world > 1 else "1 GPU",
+                       "kernel": "ens_rk4_kernel (DMMA m8n8k4 f64)",
+                       "l2": "W 8 MB + state 49 MB L2-resident by design; one launch per run"},
+            "e2e": {"value": batch_total * n * steps / e2e_s, "unit": "osc-steps/s",
+                    "h2d_bytes_per_step": 8 * (n * n + n + batch * 3 * n + batch * 11),
+                    "d2h_bytes_per_step": 8 * ens.states.size},
+            "gpu_launches": 2 * args.steps,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_TENSOR_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved / FP64_TENSOR_PEAK_TFLOPS,
+                         "traffic": None,
+                         "peak_source": "measured here: DMMA f64 microbenchmark (tools/fp64_peak.cu)",
+                         "kernel": "ens_rk4_kernel"},
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def run_ours(args, rank, world, local_rank):
@@ -366,6 +489,8 @@ def main():
     rank, world, local_rank = env_rank()
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.workload in ENSEMBLE_BATCH:
+        run_ours_ensemble(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 

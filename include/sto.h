@@ -131,6 +131,28 @@ STO_API int sto_derivative(sto_plan *plan, const double *m, const double *u, dou
 STO_API int sto_integrate(sto_plan *plan, const sto_run *run, sto_status *status, void *stream);
 STO_API int sto_plan_last_status(sto_plan *plan, sto_status *status, void *stream);
 
+/* Batched ensemble (BASELINE configs[3]): `batch` reservoirs sharing W and
+ * W_in, each with its own 11 scalars (a parameter sweep) and optionally its
+ * own drive.  The coupling of all members is one FP64 tensor-core GEMM per RK
+ * stage (DMMA); tolerance parity (<= 1e-10 at 1e3 steps), not bit-exact.
+ * On divergence: status->reserved = member, oscillator, step. */
+typedef struct {
+    int64_t batch;
+    const double *consts;          /* device (batch, 11)                          */
+    double *m;                     /* device (batch, n, 3): m0 in, final out       */
+    const double *samples;         /* device; member b reads samples + b*stride    */
+    int64_t n_samples;
+    int64_t steps_per_sample;
+    int64_t sample_member_stride;  /* elements between members' series (0 = shared) */
+    double dt;
+    int64_t steps;
+    int64_t record_stride;
+    double *states;                /* device (n_records, batch, n, 3) or NULL      */
+} sto_ensemble_run;
+
+STO_API int sto_integrate_ensemble(sto_plan *plan, const sto_ensemble_run *run,
+                                   sto_status *status, void *stream);
+
 /* Host-buffer variant (the e2e path): m, samples, states are HOST pointers;
  * copies in and out are done inside (pinned staging), then synchronises. */
 STO_API int sto_integrate_host(sto_plan *plan, double *m, const double *samples, int64_t n_samples,

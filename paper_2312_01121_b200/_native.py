@@ -49,6 +49,14 @@ class Status(ctypes.Structure):
                 ("oscillator", ctypes.c_int64), ("step", ctypes.c_int64)]
 
 
+class EnsembleRun(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int64), ("consts", ctypes.c_void_p), ("m", ctypes.c_void_p),
+                ("samples", ctypes.c_void_p), ("n_samples", ctypes.c_int64),
+                ("steps_per_sample", ctypes.c_int64), ("sample_member_stride", ctypes.c_int64),
+                ("dt", ctypes.c_double), ("steps", ctypes.c_int64),
+                ("record_stride", ctypes.c_int64), ("states", ctypes.c_void_p)]
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
@@ -69,6 +77,8 @@ SIGNATURES = {
                                       ctypes.c_void_p, ctypes.c_void_p]),
     "sto_integrate": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Run),
                                      ctypes.POINTER(Status), ctypes.c_void_p]),
+    "sto_integrate_ensemble": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(EnsembleRun),
+                                              ctypes.POINTER(Status), ctypes.c_void_p]),
     "sto_plan_last_status": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Status),
                                             ctypes.c_void_p]),
     "sto_integrate_host": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p,
@@ -189,6 +199,28 @@ class Plan:
         st = Status()
         rc = lib().sto_integrate(self._h, ctypes.byref(run),
                                  ctypes.byref(st) if sync else None, _stream_ptr(self.device))
+        check(rc, st)
+        return st
+
+    def integrate_ensemble_dev(self, m, consts, samples, steps_per_sample: int,
+                               sample_member_stride: int, dt: float, steps: int, stride: int,
+                               states) -> Status:
+        """Batched members (m: (B, n, 3), consts: (B, 11)); synchronous status."""
+        run = EnsembleRun(batch=m.shape[0], consts=consts.data_ptr(), m=m.data_ptr(),
+                          samples=samples.data_ptr(), n_samples=samples.shape[-2],
+                          steps_per_sample=int(steps_per_sample),
+                          sample_member_stride=int(sample_member_stride), dt=float(dt),
+                          steps=int(steps), record_stride=int(stride),
+                          states=states.data_ptr() if states is not None else None)
+        st = Status()
+        rc = lib().sto_integrate_ensemble(self._h, ctypes.byref(run), ctypes.byref(st),
+                                          _stream_ptr(self.device))
+        if rc == STO_E_DIVERGED:
+            from .errors import IntegrationDivergedError
+
+            err = IntegrationDivergedError(oscillator=st.oscillator, step=st.step)
+            err.member = st.reserved
+            raise err
         check(rc, st)
         return st
 

@@ -128,6 +128,40 @@ class B200Backend:
         return states
 
 
+    def integrate_ensemble_run(self, consts: np.ndarray, samples: np.ndarray,
+                               steps_per_sample: int, dt: float, steps: int, stride: int,
+                               m0: np.ndarray) -> np.ndarray:
+        """B members sharing W/W_in: consts (B, 11), m0 (B, n, 3) updated in place,
+        samples (n_samples, n_in) shared or (B, n_samples, n_in) per member.
+        Returns states (n_records, B, n, 3)."""
+        t = self._torch
+        consts = np.ascontiguousarray(consts, dtype=np.float64)
+        batch = consts.shape[0]
+        if consts.shape != (batch, 11) or m0.shape != (batch, self.n, 3):
+            raise ParameterError("ensemble expects consts (B, 11) and m0 (B, n, 3)")
+        samples = np.ascontiguousarray(samples, dtype=np.float64)
+        per_member = samples.ndim == 3
+        if per_member and samples.shape[0] != batch:
+            raise ParameterError("per-member drive must be (B, n_samples, n_in)")
+        stride_m = samples.shape[1] * samples.shape[2] if per_member else 0
+        nrec = _native.n_records(steps, stride)
+        with t.cuda.device(self._dev):
+            c_d = t.as_tensor(consts).to(self._dev)
+            m_d = t.as_tensor(np.ascontiguousarray(m0, dtype=np.float64)).to(self._dev)
+            s_d = t.as_tensor(samples).to(self._dev)
+            states_d = t.empty((nrec, batch, self.n, 3), dtype=t.float64, device=self._dev)
+            start, stop = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+            start.record()
+            self._plan.integrate_ensemble_dev(m_d, c_d, s_d, steps_per_sample, stride_m, dt,
+                                              steps, stride, states_d)
+            stop.record()
+            stop.synchronize()
+            self.last_kernel_seconds = start.elapsed_time(stop) / 1e3
+            states = states_d.cpu().numpy()
+            np.copyto(m0, m_d.cpu().numpy())
+        return states
+
+
 def make_backend(topology, params, workers=None, gpu_device=None):
     """Registry factory, signature of ref `backends/__init__.py:48-50`."""
     return B200Backend(topology, params, device=gpu_device)

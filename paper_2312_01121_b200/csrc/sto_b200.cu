@@ -12,6 +12,7 @@
 #include "../../include/sto.h"
 #include "sto_kernels.cuh"
 #include "sto_reg_kernel.cuh"
+#include "sto_ensemble_kernel.cuh"
 
 using namespace sto;
 
@@ -103,6 +104,17 @@ __global__ void permute_rows_kernel(const double *__restrict__ src, long long ld
 
 constexpr int kMaxFlags = 1024;
 
+// logical row-major (zero padded to np x np) copy of W from the device layout
+__global__ void unpermute_rows_kernel(const double *__restrict__ src, double *__restrict__ dst,
+                                      int rows, int np, ColSched cs) {
+    const long long total = (long long)np * np;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / np), c = (int)(i - (long long)r * np);
+        dst[i] = (r < rows && c < cs.n) ? src[(long long)r * cs.ldw + col_perm(cs, c)] : 0.0;
+    }
+}
+
 __global__ void reset_status_kernel(StatusDev *st, unsigned long long *bar, unsigned *flags) {
     for (int i = threadIdx.x; i < kMaxFlags; i += blockDim.x) flags[i] = 0u;
     if (threadIdx.x == 0) {
@@ -161,6 +173,12 @@ struct sto_plan {
     size_t smem = 0;
     int threads = 512;
     int team = 0;  // kReg: threads per row
+    // ensemble resources (allocated on first sto_integrate_ensemble)
+    double *ens_w = nullptr;           // np x np row-major, zero padded
+    int ens_np = 0;
+    double *ens_x = nullptr, *ens_st = nullptr;
+    size_t ens_bp = 0;                 // member capacity of ens_x / ens_st
+    unsigned long long *ens_bar = nullptr;
 };
 
 namespace {
@@ -407,6 +425,10 @@ void sto_plan_destroy(sto_plan *P) {
     cudaFree(P->bar);
     cudaFree(P->flags);
     cudaFree(P->ll);
+    cudaFree(P->ens_w);
+    cudaFree(P->ens_x);
+    cudaFree(P->ens_st);
+    cudaFree(P->ens_bar);
     cudaFree(P->status);
     delete P;
 }
@@ -484,6 +506,92 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
     }
     if (rc) return rc;
     if (status) return sto_plan_last_status(P, status, stream);
+    return STO_OK;
+}
+
+int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *status,
+                           void *stream) {
+    if (!P || !r) return fail(STO_E_PARAM, "null plan or run");
+    if (r->batch < 1 || !r->consts || !r->m || !r->samples || r->n_samples < 1 ||
+        r->steps_per_sample < 1 || r->steps < 1 || r->record_stride < 1 || !(r->dt > 0.0) ||
+        r->batch >= (1 << 20) || P->n >= (1 << 20) || r->steps >= (1LL << 23))
+        return fail(STO_E_PARAM, "bad ensemble run descriptor");
+    STO_CUDA(cudaSetDevice(P->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int np = ((P->n + kEnsRT - 1) / kEnsRT) * kEnsRT;
+    const int n_rt = np / kEnsRT;
+    const int max_cols = std::max(1, P->sm_count / n_rt);
+    if (n_rt > P->sm_count) return fail(STO_E_PARAM, "ensemble needs n <= 64 * SM count");
+    const int total_cols = (int)((r->batch + kEnsBT - 1) / kEnsBT);
+    const int cols_per_launch = std::min(max_cols, total_cols);
+    const size_t bp = (size_t)cols_per_launch * kEnsBT;
+    if (!P->ens_w) {
+        STO_CUDA(cudaMalloc(&P->ens_w, sizeof(double) * (size_t)np * np));
+        unpermute_rows_kernel<<<1184, 256, 0, s>>>(P->L.w, P->ens_w, P->n, np, P->L.cs);
+        STO_CUDA(cudaGetLastError());
+        P->ens_np = np;
+        STO_CUDA(cudaMalloc(&P->ens_bar, sizeof(unsigned long long) * 32 * 1024));
+    }
+    if (P->ens_bp < bp) {
+        cudaFree(P->ens_x);
+        cudaFree(P->ens_st);
+        P->ens_x = P->ens_st = nullptr;
+        STO_CUDA(cudaMalloc(&P->ens_x, sizeof(double) * 2 * np * bp));
+        STO_CUDA(cudaMalloc(&P->ens_st, sizeof(double) * 12 * np * bp));
+        P->ens_bp = bp;
+    }
+    const size_t smem = sizeof(double) * kEnsSmemDoubles;
+    STO_CUDA(cudaFuncSetAttribute(ens_rk4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    reset_status_kernel<<<1, 256, 0, s>>>(P->status, P->bar, P->flags);
+    STO_CUDA(cudaGetLastError());
+    for (int c0 = 0; c0 < total_cols; c0 += cols_per_launch) {
+        const int ncols = std::min(cols_per_launch, total_cols - c0);
+        EnsParams e{};
+        e.n = P->n;
+        e.np = np;
+        e.batch = (int)r->batch;
+        e.bp = (int)bp;
+        e.member0 = c0 * kEnsBT;
+        e.n_in = P->n_in;
+        e.w = P->ens_w;
+        e.w_in = P->w_in;
+        e.consts = r->consts;
+        e.m = r->m;
+        e.samples = r->samples;
+        e.sample_member_stride = r->sample_member_stride;
+        e.n_samples = r->n_samples;
+        e.sps = r->steps_per_sample;
+        e.dt = r->dt;
+        e.h2 = r->dt * 0.5;
+        e.dt6 = r->dt / 6.0;
+        e.steps = r->steps;
+        e.stride = r->record_stride;
+        e.n_records = sto_n_records(r->steps, r->record_stride);
+        e.states = r->states;
+        e.x = P->ens_x;
+        e.st = P->ens_st;
+        e.bar = P->ens_bar;
+        e.status = P->status;
+        STO_CUDA(cudaMemsetAsync(P->ens_x, 0, sizeof(double) * 2 * np * bp, s));
+        STO_CUDA(cudaMemsetAsync(P->ens_bar, 0, sizeof(unsigned long long) * 32 * 1024, s));
+        void *args[] = {(void *)&e};
+        STO_CUDA(cudaLaunchCooperativeKernel((void *)ens_rk4_kernel, dim3(n_rt * ncols),
+                                             dim3(kEnsThreads), args, smem, s));
+    }
+    if (!status) return STO_OK;
+    StatusDev h{};
+    STO_CUDA(cudaMemcpyAsync(&h, P->status, sizeof(h), cudaMemcpyDeviceToHost, s));
+    STO_CUDA(cudaStreamSynchronize(s));
+    status->diverged = h.flag;
+    status->reserved = h.flag ? (int32_t)((h.key >> 20) & 0xfffff) : -1;  // member
+    status->oscillator = h.flag ? (h.key & 0xfffff) : -1;
+    status->step = h.flag ? (h.key >> 40) : -1;
+    if (h.flag)
+        return fail(STO_E_DIVERGED, "member " + std::to_string(status->reserved) +
+                                        ": non-finite state for oscillator " +
+                                        std::to_string(status->oscillator) + " at step " +
+                                        std::to_string(status->step));
     return STO_OK;
 }
 
