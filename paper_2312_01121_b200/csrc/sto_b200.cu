@@ -106,11 +106,11 @@ constexpr int kMaxFlags = 1024;
 
 // logical row-major (zero padded to np x np) copy of W from the device layout
 __global__ void unpermute_rows_kernel(const double *__restrict__ src, double *__restrict__ dst,
-                                      int rows, int np, ColSched cs) {
-    const long long total = (long long)np * np;
+                                      int rows, int np, int kp, ColSched cs) {
+    const long long total = (long long)np * kp;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(i / np), c = (int)(i - (long long)r * np);
+        const int r = (int)(i / kp), c = (int)(i - (long long)r * kp);
         dst[i] = (r < rows && c < cs.n) ? src[(long long)r * cs.ldw + col_perm(cs, c)] : 0.0;
     }
 }
@@ -519,6 +519,7 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
     STO_CUDA(cudaSetDevice(P->device));
     cudaStream_t s = (cudaStream_t)stream;
     const int np = ((P->n + kEnsRT - 1) / kEnsRT) * kEnsRT;
+    const int kp = ((P->n + kEnsKC - 1) / kEnsKC) * kEnsKC;
     const int n_rt = np / kEnsRT;
     const int max_cols = std::max(1, P->sm_count / n_rt);
     if (n_rt > P->sm_count) return fail(STO_E_PARAM, "ensemble needs n <= 64 * SM count");
@@ -526,8 +527,8 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
     const int cols_per_launch = std::min(max_cols, total_cols);
     const size_t bp = (size_t)cols_per_launch * kEnsBT;
     if (!P->ens_w) {
-        STO_CUDA(cudaMalloc(&P->ens_w, sizeof(double) * (size_t)np * np));
-        unpermute_rows_kernel<<<1184, 256, 0, s>>>(P->L.w, P->ens_w, P->n, np, P->L.cs);
+        STO_CUDA(cudaMalloc(&P->ens_w, sizeof(double) * (size_t)np * kp));
+        unpermute_rows_kernel<<<1184, 256, 0, s>>>(P->L.w, P->ens_w, P->n, np, kp, P->L.cs);
         STO_CUDA(cudaGetLastError());
         P->ens_np = np;
         STO_CUDA(cudaMalloc(&P->ens_bar, sizeof(unsigned long long) * 32 * 1024));
@@ -536,8 +537,8 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
         cudaFree(P->ens_x);
         cudaFree(P->ens_st);
         P->ens_x = P->ens_st = nullptr;
-        STO_CUDA(cudaMalloc(&P->ens_x, sizeof(double) * 2 * np * bp));
-        STO_CUDA(cudaMalloc(&P->ens_st, sizeof(double) * 12 * np * bp));
+        STO_CUDA(cudaMalloc(&P->ens_x, sizeof(double) * 2 * std::max(np, kp) * bp));
+        STO_CUDA(cudaMalloc(&P->ens_st, sizeof(double) * kEnsState * np * bp));
         P->ens_bp = bp;
     }
     const size_t smem = sizeof(double) * kEnsSmemDoubles;
@@ -550,6 +551,7 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
         EnsParams e{};
         e.n = P->n;
         e.np = np;
+        e.kp = kp;
         e.batch = (int)r->batch;
         e.bp = (int)bp;
         e.member0 = c0 * kEnsBT;
@@ -573,7 +575,7 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
         e.st = P->ens_st;
         e.bar = P->ens_bar;
         e.status = P->status;
-        STO_CUDA(cudaMemsetAsync(P->ens_x, 0, sizeof(double) * 2 * np * bp, s));
+        STO_CUDA(cudaMemsetAsync(P->ens_x, 0, sizeof(double) * 2 * std::max(np, kp) * bp, s));
         STO_CUDA(cudaMemsetAsync(P->ens_bar, 0, sizeof(unsigned long long) * 32 * 1024, s));
         void *args[] = {(void *)&e};
         STO_CUDA(cudaLaunchCooperativeKernel((void *)ens_rk4_kernel, dim3(n_rt * ncols),
@@ -689,6 +691,10 @@ int sto_tree_matvec(int device, int64_t rows, int64_t cols, const double *a, int
 }
 
 #ifdef STO_TIMELINE
+STO_API int sto_debug_ens_timeline(unsigned long long *out, int count) {
+    STO_CUDA(cudaMemcpyFromSymbol(out, g_ens_timeline, sizeof(unsigned long long) * count));
+    return STO_OK;
+}
 STO_API int sto_debug_timeline(unsigned long long *out, int count) {
     STO_CUDA(cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * count));
     return STO_OK;
