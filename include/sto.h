@@ -71,6 +71,13 @@ typedef struct {
     double consts[STO_N_CONSTS];
     int device;           /* CUDA device ordinal                                 */
     int flags;            /* STO_PLAN_* bits                                     */
+    /* Row sharding (multi-GPU).  world <= 1: unsharded, the rest is ignored.
+     * Otherwise this plan owns global rows [row_begin, row_begin + row_count)
+     * and w_cp / w_in point at THOSE rows (w_cp still has n columns).        */
+    int64_t row_begin;
+    int64_t row_count;
+    int32_t world;
+    int32_t rank;
 } sto_plan_desc;
 
 /* Force a kernel family (testing / benchmarking); default = automatic. */
@@ -152,6 +159,25 @@ typedef struct {
 
 STO_API int sto_integrate_ensemble(sto_plan *plan, const sto_ensemble_run *run,
                                    sto_status *status, void *stream);
+
+/* Row-sharded multi-GPU (one process per GPU).  Each rank exports the IPC
+ * handle of its exchange buffer (64 bytes, cudaIpcMemHandle_t), the caller
+ * all-gathers them (e.g. torch.distributed) and connects; sto_integrate then
+ * runs this rank's rows and all-gathers the stage x-vector over NVLink inside
+ * the persistent kernel (peer stores + epoch flags, no NCCL call per stage).
+ * run->m must hold the full (n, 3) initial state on every rank; on return it
+ * holds this rank's rows of the final state, and states (n_records, n, 3)
+ * this rank's rows.  All ranks must call sto_integrate with the same run
+ * parameters, and finish a run before any rank starts the next one. */
+STO_API int sto_plan_exchange_handle(sto_plan *plan, void *handle_out, int64_t handle_bytes);
+STO_API int sto_plan_connect(sto_plan *plan, const void *handles, int32_t world);
+
+/* Test / single-GPU mode: `world` sharded plans of ONE device act as logical
+ * ranks of one persistent launch, exchanging through plain device buffers
+ * with exactly the multi-GPU protocol. */
+STO_API int sto_plan_connect_local(sto_plan **plans, int32_t world);
+STO_API int sto_integrate_group(sto_plan **plans, int32_t world, const sto_run *run,
+                                sto_status *status, void *stream);
 
 /* Host-buffer variant (the e2e path): m, samples, states are HOST pointers;
  * copies in and out are done inside (pinned staging), then synchronises. */

@@ -34,7 +34,9 @@ class PlanDesc(ctypes.Structure):
                 ("w_cp", ctypes.c_void_p), ("ld_cp", ctypes.c_int64),
                 ("w_in", ctypes.c_void_p), ("ld_in", ctypes.c_int64),
                 ("consts", ctypes.c_double * 11), ("device", ctypes.c_int),
-                ("flags", ctypes.c_int)]
+                ("flags", ctypes.c_int), ("row_begin", ctypes.c_int64),
+                ("row_count", ctypes.c_int64), ("world", ctypes.c_int32),
+                ("rank", ctypes.c_int32)]
 
 
 class Run(ctypes.Structure):
@@ -81,6 +83,13 @@ SIGNATURES = {
                                               ctypes.POINTER(Status), ctypes.c_void_p]),
     "sto_plan_last_status": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Status),
                                             ctypes.c_void_p]),
+    "sto_plan_exchange_handle": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_int64]),
+    "sto_plan_connect": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]),
+    "sto_plan_connect_local": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32]),
+    "sto_integrate_group": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                           ctypes.POINTER(Run), ctypes.POINTER(Status),
+                                           ctypes.c_void_p]),
     "sto_integrate_host": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p,
                                           ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
                                           ctypes.c_int64, ctypes.c_int64, _c_double_p,
@@ -153,17 +162,26 @@ class Plan:
     """Owns a device-resident W layout + launch configuration (sto_plan)."""
 
     def __init__(self, w_cp: np.ndarray, w_in: np.ndarray, consts, device: int = 0,
-                 flags: int = 0):
+                 flags: int = 0, shard: tuple[int, int, int, int] | None = None):
+        """shard = (row_begin, row_count, world, rank): w_cp / w_in hold only the
+        shard's rows (row_count x n and row_count x n_in)."""
         w_cp = np.ascontiguousarray(w_cp, dtype=np.float64)
         w_in = np.ascontiguousarray(w_in, dtype=np.float64)
-        if w_cp.ndim != 2 or w_cp.shape[0] != w_cp.shape[1]:
+        n = w_cp.shape[1]
+        rows = w_cp.shape[0]
+        if w_cp.ndim != 2 or (shard is None and rows != n):
             raise ParameterError("coupling matrix must be square")
-        if w_in.ndim != 2 or w_in.shape[0] != w_cp.shape[0]:
+        if w_in.ndim != 2 or w_in.shape[0] != rows:
             raise ParameterError("input weights must be (n, n_in)")
-        self.n, self.n_in = w_cp.shape[0], w_in.shape[1]
+        self.n, self.n_in = n, w_in.shape[1]
         self.device = int(device)
+        self.shard = shard
         d = PlanDesc(n=self.n, n_in=self.n_in, w_cp=w_cp.ctypes.data, ld_cp=self.n,
                      w_in=w_in.ctypes.data, ld_in=self.n_in, device=self.device, flags=flags)
+        if shard is not None:
+            d.row_begin, d.row_count, d.world, d.rank = (int(v) for v in shard)
+            if d.row_count != rows:
+                raise ParameterError("shard row_count must equal the rows passed")
         for i, v in enumerate(consts):
             d.consts[i] = float(v)
         h = ctypes.c_void_p()
@@ -224,6 +242,15 @@ class Plan:
         check(rc, st)
         return st
 
+    def exchange_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        check(lib().sto_plan_exchange_handle(self._h, buf, 64))
+        return buf.raw
+
+    def connect(self, handles: list[bytes]) -> None:
+        blob = b"".join(handles)
+        check(lib().sto_plan_connect(self._h, blob, len(handles)))
+
     def last_status(self) -> Status:
         st = Status()
         check(lib().sto_plan_last_status(self._h, ctypes.byref(st), _stream_ptr(self.device)),
@@ -247,3 +274,22 @@ def tree_matvec(matrix, vec, out=None, device: int | None = None):
         return res
     np.copyto(out, res)
     return out
+
+
+def connect_local(plans: list["Plan"]) -> None:
+    arr = (ctypes.c_void_p * len(plans))(*[p._h.value for p in plans])
+    check(lib().sto_plan_connect_local(arr, len(plans)))
+
+
+def integrate_group(plans: list["Plan"], m, samples, steps_per_sample: int, dt: float,
+                    steps: int, stride: int, states) -> Status:
+    """Logical ranks of one device in one persistent launch (synchronous)."""
+    arr = (ctypes.c_void_p * len(plans))(*[p._h.value for p in plans])
+    run = Run(m=m.data_ptr(), samples=samples.data_ptr(), n_samples=samples.shape[0],
+              steps_per_sample=int(steps_per_sample), dt=float(dt), steps=int(steps),
+              record_stride=int(stride), states=states.data_ptr() if states is not None else None)
+    st = Status()
+    rc = lib().sto_integrate_group(arr, len(plans), ctypes.byref(run), ctypes.byref(st),
+                                   _stream_ptr(plans[0].device))
+    check(rc, st)
+    return st

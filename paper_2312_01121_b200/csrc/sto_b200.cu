@@ -173,6 +173,17 @@ struct sto_plan {
     size_t smem = 0;
     int threads = 512;
     int team = 0;  // kReg: threads per row
+    // row sharding (world > 1)
+    int world = 1, rank = 0;
+    long long row_begin = 0;
+    int rows = 0;                       // rows owned (== n unsharded)
+    double *exch = nullptr;             // [2][ldw] receive buffer + flags (IPC-exportable)
+    unsigned long long *exch_flags = nullptr;
+    double *xbuf_of[kMaxRanks] = {};
+    unsigned long long *flags_of[kMaxRanks] = {};
+    void *ipc_opened[kMaxRanks] = {};
+    bool connected = false;
+    unsigned long long epoch_base = 0;  // monotonic epochs across launches
     // ensemble resources (allocated on first sto_integrate_ensemble)
     double *ens_w = nullptr;           // np x np row-major, zero padded
     int ens_np = 0;
@@ -209,6 +220,27 @@ int launch_grid(const KParams &p, int grid, size_t smem, bool cooperative, cudaS
         STO_CUDA(cudaGetLastError());
     }
     return STO_OK;
+}
+
+template <WSrc S>
+int launch_multi(const KParams &p, int grid, size_t smem, cudaStream_t stream) {
+    auto fn = grid_rk4_kernel<S, false, true>;
+    STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    void *args[] = {(void *)&p};
+    STO_CUDA(cudaLaunchCooperativeKernel((void *)fn, dim3(grid), dim3(kThreads), args, smem, stream));
+    return STO_OK;
+}
+
+ShardInfo shard_info(const sto_plan *P) {
+    ShardInfo s{};
+    s.w = P->L.w;
+    s.w_in = P->w_in;
+    s.row_begin = P->row_begin;
+    s.rows = P->rows;
+    s.bar = P->bar;
+    s.xbuf = P->exch;
+    s.flags = P->exch_flags;
+    return s;
 }
 
 template <int T, int C, bool SINGLE>
@@ -314,6 +346,10 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     *out = nullptr;
     if (d->n < 1 || d->n_in < 1 || d->n > (1 << 24) || d->n_in > (1 << 20))
         return fail(STO_E_PARAM, "n and n_in must be >= 1");
+    const bool sharded = d->world > 1;
+    if (sharded && (d->world > kMaxRanks || d->rank < 0 || d->rank >= d->world ||
+                    d->row_begin < 0 || d->row_count < 1 || d->row_begin + d->row_count > d->n))
+        return fail(STO_E_PARAM, "bad row shard (world <= 8, 0 <= rank < world, rows inside n)");
     if (!d->w_cp || !d->w_in || d->ld_cp < d->n || d->ld_in < d->n_in)
         return fail(STO_E_PARAM, "bad W / W_in pointers or leading dimensions");
     cudaDeviceProp prop;
@@ -326,6 +362,10 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     P->l2_bytes = prop.l2CacheSize;
     P->n = (int)d->n;
     P->n_in = (int)d->n_in;
+    P->world = sharded ? d->world : 1;
+    P->rank = sharded ? d->rank : 0;
+    P->row_begin = sharded ? d->row_begin : 0;
+    P->rows = sharded ? (int)d->row_count : (int)d->n;
     const double *k = d->consts;
     P->c = Consts{k[0], k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8], k[9], k[10]};
 
@@ -336,9 +376,20 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     cudaStream_t s = nullptr;
     const int n = P->n;
     const int blk_hint = n >= 8192 ? 2048 : 512;
-    if (int rc = upload_layout(P->L, n, n, d->w_cp, d->ld_cp, blk_hint, s)) return bail(rc);
+    if (int rc = upload_layout(P->L, P->rows, n, d->w_cp, d->ld_cp, blk_hint, s)) return bail(rc);
     const ColSched &cs = P->L.cs;
-    if (cudaMalloc(&P->w_in, sizeof(double) * (size_t)n * d->n_in) != cudaSuccess ||
+    if (sharded) {
+        const size_t xb = sizeof(double) * 2 * (size_t)cs.ldw;
+        const size_t fb = sizeof(unsigned long long) * kMaxRanks * kFlagSlot;
+        if (cudaMalloc(&P->exch, xb + fb) != cudaSuccess)
+            return bail(fail(STO_E_NOMEM, "exchange buffer allocation failed"));
+        if (cudaMemset(P->exch, 0, xb + fb) != cudaSuccess)
+            return bail(fail(STO_E_CUDA, "exchange buffer init failed"));
+        P->exch_flags = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(P->exch) + xb);
+        P->xbuf_of[P->rank] = P->exch;
+        P->flags_of[P->rank] = P->exch_flags;
+    }
+    if (cudaMalloc(&P->w_in, sizeof(double) * (size_t)P->rows * d->n_in) != cudaSuccess ||
         cudaMalloc(&P->xbuf, sizeof(double) * 2 * (size_t)cs.ldw) != cudaSuccess ||
         cudaMalloc(&P->bar, 64) != cudaSuccess ||
         cudaMalloc(&P->flags, sizeof(unsigned) * kMaxFlags) != cudaSuccess ||
@@ -346,7 +397,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         cudaMalloc(&P->status, sizeof(StatusDev)) != cudaSuccess)
         return bail(fail(STO_E_NOMEM, "device allocation failed"));
     if (cudaMemcpy2D(P->w_in, sizeof(double) * d->n_in, d->w_in, sizeof(double) * d->ld_in,
-                     sizeof(double) * d->n_in, n, cudaMemcpyDefault) != cudaSuccess ||
+                     sizeof(double) * d->n_in, P->rows, cudaMemcpyDefault) != cudaSuccess ||
         cudaMemset(P->xbuf, 0, sizeof(double) * 2 * (size_t)cs.ldw) != cudaSuccess)
         return bail(fail(STO_E_CUDA, "W_in upload failed"));
 
@@ -357,7 +408,24 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     const size_t single_smem = grid_smem(n, cs, cs.ldw, true);
     int pw = 32;
     while (pw < n) pw <<= 1;
-    if (n <= 32 && !(fl & STO_PLAN_NO_TINY) && !forced) {
+    if (sharded) {
+        // sharded plans always use the grid kernel (MULTI); rows = this shard
+        const int g = std::min(P->sm_count, P->rows);
+        P->rows_cap = (P->rows + g - 1) / g;
+        const size_t res_smem = grid_smem(P->rows_cap, cs, cs.ldw, true);
+        if (!(fl & STO_PLAN_FORCE_STREAM) && res_smem <= kSmemBudget) {
+            P->kind = kResident;
+            P->chunk_cols = cs.ldw;
+            P->smem = res_smem;
+        } else {
+            P->kind = kStream;
+            P->chunk_cols = choose_chunk(cs, P->rows_cap, false);
+            P->smem = grid_smem(P->rows_cap, cs, P->chunk_cols, false);
+            const double wbytes = (double)P->rows * cs.ldw * sizeof(double);
+            P->stream_evict_first = wbytes > 0.6 * (double)P->l2_bytes;
+        }
+        P->grid = g;
+    } else if (n <= 32 && !(fl & STO_PLAN_NO_TINY) && !forced) {
         P->kind = kTiny;
         P->grid = 1;
         P->threads = 32;
@@ -419,6 +487,9 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
 void sto_plan_destroy(sto_plan *P) {
     if (!P) return;
     cudaSetDevice(P->device);
+    for (int q = 0; q < kMaxRanks; ++q)
+        if (P->ipc_opened[q]) cudaIpcCloseMemHandle(P->ipc_opened[q]);
+    cudaFree(P->exch);
     cudaFree(P->L.w);
     cudaFree(P->w_in);
     cudaFree(P->xbuf);
@@ -447,6 +518,7 @@ int sto_plan_get_info(const sto_plan *P, sto_plan_info *info) {
 
 int sto_derivative(sto_plan *P, const double *m, const double *u, double *out, void *stream) {
     if (!P || !m || !u || !out) return fail(STO_E_PARAM, "null argument");
+    if (P->world > 1) return fail(STO_E_PARAM, "sto_derivative needs an unsharded plan");
     STO_CUDA(cudaSetDevice(P->device));
     cudaStream_t s = (cudaStream_t)stream;
     KParams p = base_params(P);
@@ -489,6 +561,25 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
     reset_status_kernel<<<1, 256, 0, s>>>(P->status, P->bar, P->flags);
     STO_CUDA(cudaGetLastError());
     int rc = STO_OK;
+    if (P->world > 1) {
+        if (!P->connected) return fail(STO_E_PARAM, "sharded plan is not connected to its peers");
+        p.mp.world = P->world;
+        p.mp.rank_base = P->rank;
+        p.mp.ctas_per_rank = P->grid;
+        p.mp.epoch_base = P->epoch_base;
+        p.mp.sh[0] = shard_info(P);
+        for (int q = 0; q < P->world; ++q) {
+            p.mp.xbuf_of[q] = P->xbuf_of[q];
+            p.mp.flags_of[q] = P->flags_of[q];
+        }
+        rc = P->kind == kResident ? launch_multi<WSrc::Shared>(p, P->grid, P->smem, s)
+             : P->stream_evict_first ? launch_multi<WSrc::GlobalStream>(p, P->grid, P->smem, s)
+                                     : launch_multi<WSrc::GlobalL2>(p, P->grid, P->smem, s);
+        P->epoch_base += 4ull * (unsigned long long)r->steps;
+        if (rc) return rc;
+        if (status) return sto_plan_last_status(P, status, stream);
+        return STO_OK;
+    }
     switch (P->kind) {
         case kTiny: rc = launch_tiny(p, P->n, s); break;
         case kReg: {
@@ -594,6 +685,108 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
                                         ": non-finite state for oscillator " +
                                         std::to_string(status->oscillator) + " at step " +
                                         std::to_string(status->step));
+    return STO_OK;
+}
+
+int sto_plan_exchange_handle(sto_plan *P, void *out, int64_t bytes) {
+    if (!P || !out || bytes < (int64_t)sizeof(cudaIpcMemHandle_t) || P->world < 2)
+        return fail(STO_E_PARAM, "exchange handle needs a sharded plan and a 64-byte buffer");
+    STO_CUDA(cudaSetDevice(P->device));
+    cudaIpcMemHandle_t h;
+    STO_CUDA(cudaIpcGetMemHandle(&h, P->exch));
+    std::memcpy(out, &h, sizeof(h));
+    return STO_OK;
+}
+
+int sto_plan_connect(sto_plan *P, const void *handles, int32_t world) {
+    if (!P || !handles || world != P->world) return fail(STO_E_PARAM, "bad connect arguments");
+    STO_CUDA(cudaSetDevice(P->device));
+    const size_t xb = sizeof(double) * 2 * (size_t)P->L.cs.ldw;
+    for (int q = 0; q < world; ++q) {
+        if (q == P->rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const char *>(handles) + q * sizeof(h), sizeof(h));
+        void *ptr = nullptr;
+        STO_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        P->ipc_opened[q] = ptr;
+        P->xbuf_of[q] = static_cast<double *>(ptr);
+        P->flags_of[q] = reinterpret_cast<unsigned long long *>(static_cast<char *>(ptr) + xb);
+    }
+    P->connected = true;
+    return STO_OK;
+}
+
+int sto_plan_connect_local(sto_plan **plans, int32_t world) {
+    if (!plans || world < 2 || world > kMaxRanks) return fail(STO_E_PARAM, "bad local group");
+    for (int q = 0; q < world; ++q) {
+        if (!plans[q] || plans[q]->world != world || plans[q]->rank != q ||
+            plans[q]->device != plans[0]->device || plans[q]->n != plans[0]->n ||
+            plans[q]->L.cs.ldw != plans[0]->L.cs.ldw)
+            return fail(STO_E_PARAM, "local group plans must be ranks 0..world-1 of one device");
+    }
+    for (int q = 0; q < world; ++q) {
+        for (int o = 0; o < world; ++o) {
+            plans[q]->xbuf_of[o] = plans[o]->exch;
+            plans[q]->flags_of[o] = plans[o]->exch_flags;
+        }
+        plans[q]->connected = true;
+    }
+    return STO_OK;
+}
+
+int sto_integrate_group(sto_plan **plans, int32_t world, const sto_run *r, sto_status *status,
+                        void *stream) {
+    if (!plans || world < 2 || world > kMaxRanks || !r) return fail(STO_E_PARAM, "bad group");
+    sto_plan *P0 = plans[0];
+    for (int q = 0; q < world; ++q)
+        if (!plans[q] || !plans[q]->connected || plans[q]->world != world ||
+            plans[q]->kind != P0->kind || plans[q]->smem > P0->smem ||
+            plans[q]->stream_evict_first != P0->stream_evict_first ||
+            plans[q]->chunk_cols != P0->chunk_cols)
+            return fail(STO_E_PARAM, "group plans must be connected shards with one kernel family");
+    if (!r->m || !r->samples || r->n_samples < 1 || r->steps_per_sample < 1 || r->steps < 1 ||
+        r->record_stride < 1 || !(r->dt > 0.0))
+        return fail(STO_E_PARAM, "bad run descriptor");
+    STO_CUDA(cudaSetDevice(P0->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    KParams p = base_params(P0);
+    p.mode = kIntegrate;
+    p.m = r->m;
+    p.samples = r->samples;
+    p.n_samples = r->n_samples;
+    p.sps = r->steps_per_sample;
+    p.dt = r->dt;
+    p.h2 = r->dt * 0.5;
+    p.dt6 = r->dt / 6.0;
+    p.steps = r->steps;
+    p.stride = r->record_stride;
+    p.n_records = sto_n_records(r->steps, r->record_stride);
+    p.states = r->states;
+    int cap = 1;
+    const int per = P0->sm_count / world;  // CTAs per logical rank
+    for (int q = 0; q < world; ++q) cap = std::max(cap, (plans[q]->rows + per - 1) / per);
+    p.rows_cap = cap;
+    p.chunk_cols = P0->chunk_cols;
+    const size_t smem = grid_smem(cap, P0->L.cs, p.chunk_cols, P0->kind == kResident);
+    if (smem > kSmemBudget) return fail(STO_E_PARAM, "group shard does not fit shared memory");
+    p.mp.world = world;
+    p.mp.rank_base = 0;
+    p.mp.ctas_per_rank = per;
+    p.mp.epoch_base = P0->epoch_base;
+    for (int q = 0; q < world; ++q) {
+        p.mp.sh[q] = shard_info(plans[q]);
+        p.mp.xbuf_of[q] = plans[q]->exch;
+        p.mp.flags_of[q] = plans[q]->exch_flags;
+        if (plans[q]->epoch_base != P0->epoch_base) return fail(STO_E_PARAM, "group epochs differ");
+        reset_status_kernel<<<1, 256, 0, s>>>(plans[q]->status, plans[q]->bar, plans[q]->flags);
+    }
+    p.status = P0->status;
+    int rc = P0->kind == kResident ? launch_multi<WSrc::Shared>(p, per * world, smem, s)
+             : P0->stream_evict_first ? launch_multi<WSrc::GlobalStream>(p, per * world, smem, s)
+                                      : launch_multi<WSrc::GlobalL2>(p, per * world, smem, s);
+    for (int q = 0; q < world; ++q) plans[q]->epoch_base += 4ull * (unsigned long long)r->steps;
+    if (rc) return rc;
+    if (status) return sto_plan_last_status(P0, status, stream);
     return STO_OK;
 }
 

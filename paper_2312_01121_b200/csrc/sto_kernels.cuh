@@ -36,6 +36,42 @@ __device__ __forceinline__ void report_divergence(StatusDev *st, long long step,
 
 enum KernelMode : int { kIntegrate = 0, kDerivative = 1, kMatvec = 2 };
 
+// ----------------------------------------------------------------------------
+// Row-sharded multi-rank mode (MULTI): rank q owns global rows
+// [row_begin, row_begin + rows) with its own W shard; after every RK stage each
+// CTA stores its rows' x straight into EVERY rank's receive buffer (peer
+// pointers: CUDA-IPC-mapped NVLink memory on a multi-GPU box, or plain device
+// buffers when several logical ranks share one GPU for testing), then
+//   local barrier (counter) -> leader raises its epoch flag in every rank's
+//   flag array (st.release.sys) -> all CTAs wait for all `world` flags.
+// Epochs are 64-bit and monotonic across launches, so flags are never reset
+// while a peer may be writing them.
+// ----------------------------------------------------------------------------
+constexpr int kMaxRanks = 8;
+constexpr int kFlagSlot = 32;  // u64 words between flag slots (256 B)
+
+struct ShardInfo {
+    const double *w;          // rows x ldw, device layout (this rank's rows)
+    const double *w_in;       // rows x n_in
+    long long row_begin;
+    int rows;
+    int pad;
+    unsigned long long *bar;  // this rank's local barrier counter
+    double *xbuf;             // this rank's receive buffer [2][ldw]
+    unsigned long long *flags;  // this rank's flag array [world][kFlagSlot]
+};
+
+struct MultiParams {
+    int world;               // ranks in the job
+    int rank_base;           // first rank hosted by this launch
+    int ctas_per_rank;
+    int pad;
+    unsigned long long epoch_base;  // monotonic across launches
+    ShardInfo sh[kMaxRanks];        // ranks hosted by this launch
+    double *xbuf_of[kMaxRanks];     // every rank's receive buffer (peer pointers)
+    unsigned long long *flags_of[kMaxRanks];
+};
+
 struct KParams {
     ColSched cs;
     Consts c;
@@ -58,6 +94,7 @@ struct KParams {
     double *xbuf;           // 2 x ldw published stage x (physical layout), +0.0 padded
     unsigned long long *bar;
     StatusDev *status;
+    MultiParams mp;         // MULTI only
 };
 
 // ----------------------------------------------------------------------------
@@ -76,6 +113,46 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long
         __threadfence();
     }
     __syncthreads();
+}
+
+// local counter barrier, then epoch flags across ranks (see MultiParams)
+__device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInfo &sh, int rank,
+                                           int lcta, unsigned long long local_target,
+                                           unsigned long long epoch, bool record_stage,
+                                           const StatusDev *status, volatile int *sflag) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("fence.sc.sys;" ::: "memory");  // our peer stores are system-visible
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(sh.bar) : "memory");
+        unsigned long long v;
+        do {
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(sh.bar) : "memory");
+        } while (v < local_target);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (lcta == 0) {
+            // every local CTA has passed the barrier, so a divergence on this
+            // recording step is already in the (local) status
+            const bool diverged = record_stage && *((volatile const int32_t *)&status->flag) != 0;
+            const unsigned long long f = epoch | (diverged ? (1ull << 63) : 0ull);
+            for (int q = 0; q < mp.world; ++q)
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(mp.flags_of[q] + (size_t)rank * kFlagSlot),
+                             "l"(f)
+                             : "memory");
+        }
+    }
+    if (threadIdx.x < mp.world) {
+        unsigned long long f;
+        do {
+            asm volatile("ld.relaxed.sys.global.u64 %0, [%1];"
+                         : "=l"(f)
+                         : "l"(sh.flags + (size_t)threadIdx.x * kFlagSlot)
+                         : "memory");
+        } while ((f & ~(1ull << 63)) < epoch);
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        if (f >> 63) *sflag = 1;
+    }
+    __syncthreads();
+    return *sflag != 0;
 }
 
 __device__ __forceinline__ int row_lo(int b, int g, int rows) {
@@ -107,14 +184,23 @@ struct RowState {
 enum { kSlotM = 0, kSlotS = 1, kSlotAcc = 2, kSlotK3 = 3 };
 
 // Shared layout: [X window | W rows (resident) | nodes | row state | flags]
-template <WSrc S, bool SINGLE>
+template <WSrc S, bool SINGLE, bool MULTI = false>
 __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant__ KParams p) {
     extern __shared__ __align__(16) double smem[];
     const ColSched &cs = p.cs;
-    const int G = gridDim.x;
-    const int b = blockIdx.x;
-    const int r0 = row_lo(b, G, p.rows);
-    const int nrow = row_lo(b + 1, G, p.rows) - r0;
+    // rank view: MULTI hosts one or more logical ranks, each on its own CTAs
+    const int lr = MULTI ? (int)(blockIdx.x / p.mp.ctas_per_rank) : 0;
+    const ShardInfo &sh = p.mp.sh[lr];
+    const int rank = MULTI ? p.mp.rank_base + lr : 0;
+    const int G = MULTI ? p.mp.ctas_per_rank : gridDim.x;
+    const int b = MULTI ? (int)(blockIdx.x % p.mp.ctas_per_rank) : blockIdx.x;
+    const int rows = MULTI ? sh.rows : p.rows;             // rows owned by this rank
+    const long long rb = MULTI ? sh.row_begin : 0;         // global index of local row 0
+    const double *Wg = MULTI ? sh.w : p.w;
+    const double *Win = MULTI ? sh.w_in : p.w_in;
+    double *xrecv = MULTI ? sh.xbuf : p.xbuf;
+    const int r0 = row_lo(b, G, rows);
+    const int nrow = row_lo(b + 1, G, rows) - r0;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
@@ -128,7 +214,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
 
     // ---- prologue: resident W rows, own state, initial record -------------
     if constexpr (S == WSrc::Shared) {
-        const double2 *src = reinterpret_cast<const double2 *>(p.w + (size_t)r0 * cs.ldw);
+        const double2 *src = reinterpret_cast<const double2 *>(Wg + (size_t)r0 * cs.ldw);
         double2 *dst = reinterpret_cast<double2 *>(wres);
         const int n2 = nrow * cs.ldw / 2;
         for (int i = threadIdx.x; i < n2; i += blockDim.x) dst[i] = src[i];
@@ -136,11 +222,11 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
     const bool integrate = p.mode == kIntegrate;
     if (p.mode != kMatvec) {
         for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
-            const double *mm = p.m + 3 * (size_t)(r0 + r);
+            const double *mm = p.m + 3 * (size_t)(rb + r0 + r);
             const V3 v{mm[0], mm[1], mm[2]};
             rs.put(kSlotM, r, v);
             if (integrate && p.states) {
-                double *st = p.states + 3 * (size_t)(r0 + r);
+                double *st = p.states + 3 * (size_t)(rb + r0 + r);
                 st[0] = v.x;
                 st[1] = v.y;
                 st[2] = v.z;
@@ -176,7 +262,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
                         xs[col_perm(cs, k) - x_base] = v;
                     }
                 } else {
-                    const double *src = p.xbuf + (size_t)(e & 1) * cs.ldw + x_base;
+                    const double *src = xrecv + (size_t)((MULTI ? p.mp.epoch_base + e : e) & 1) * cs.ldw + x_base;
                     const double2 *src2 = reinterpret_cast<const double2 *>(src);
                     double2 *dst2 = reinterpret_cast<double2 *>(xs);
 #pragma unroll 4
@@ -191,7 +277,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
                 const int r = unit / bcount;
                 const int bb = bfirst + unit % bcount;
                 const double *wrow = (S == WSrc::Shared) ? wres + (size_t)r * cs.ldw
-                                                         : p.w + (size_t)(r0 + r) * cs.ldw;
+                                                         : Wg + (size_t)(r0 + r) * cs.ldw;
                 const double node = block_node<S>(cs, bb, wrow, xs, x_base, lane);
                 if (lane == 0) nodes[(size_t)r * cs.nblocks + bb] = node;
             }
@@ -201,9 +287,11 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
         const long long rec = (integrate && stage == 3)
                                   ? record_index(step, p.stride, p.steps, p.n_records)
                                   : -1;
-        double *xnext = SINGLE ? xs : p.xbuf + (size_t)((e + 1) & 1) * cs.ldw;
+        const size_t par_next = (size_t)((MULTI ? p.mp.epoch_base + e + 1 : e + 1) & 1) * cs.ldw;
+        double *xnext = SINGLE ? xs : xrecv + par_next;
         for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
-            const int k = r0 + r;
+            const int kl = r0 + r;          // local row (W shard, W_in shard)
+            const int k = (int)(rb + kl);   // global oscillator index
             const double cp = tree_inplace(nodes + (size_t)r * cs.nblocks, cs.nblocks);
             if (p.mode == kMatvec) {
                 p.out[k] = cp;
@@ -211,8 +299,8 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
             }
             if (stage == 0) {
                 rs.cin(r) = (p.n_in == 1)
-                                ? rmul(p.w_in[k], u[0])
-                                : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
+                                ? rmul(Win[kl], u[0])
+                                : tree_dot_stream(Win + (size_t)kl * p.n_in, u, p.n_in);
             }
             const V3 mk = rs.get(kSlotM, r);
             const V3 cur = (stage == 0) ? mk : rs.get(kSlotS, r);
@@ -249,14 +337,19 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
                         report_divergence(p.status, step, k);
                         *sflag = 1;
                     } else if (p.states) {
-                        double *st = p.states + ((size_t)rec * p.rows + k) * 3;
+                        double *st = p.states + ((size_t)rec * cs.n + k) * 3;
                         st[0] = mn.x;
                         st[1] = mn.y;
                         st[2] = mn.z;
                     }
                 }
             }
-            xnext[col_perm(cs, k)] = xpub;
+            if constexpr (MULTI) {
+                const int pos = col_perm(cs, k);
+                for (int q = 0; q < p.mp.world; ++q) p.mp.xbuf_of[q][par_next + pos] = xpub;
+            } else {
+                xnext[col_perm(cs, k)] = xpub;
+            }
         }
         if (!integrate) break;
         if (e + 1 == total_stages) break;
@@ -264,6 +357,10 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
         if constexpr (SINGLE) {
             __syncthreads();
             if (*sflag) break;
+        } else if constexpr (MULTI) {
+            if (multi_sync(p.mp, sh, rank, b, (unsigned long long)(e + 1) * G,
+                           p.mp.epoch_base + e + 1, stage == 3 && rec >= 0, p.status, sflag))
+                break;
         } else {
             grid_sync(p.bar, (unsigned long long)(e + 1) * G);
             if (stage == 3 && rec >= 0) {
@@ -284,7 +381,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
         __syncthreads();
         for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
             const V3 v = rs.get(kSlotM, r);
-            double *mm = p.m + 3 * (size_t)(r0 + r);
+            double *mm = p.m + 3 * (size_t)(rb + r0 + r);
             mm[0] = v.x;
             mm[1] = v.y;
             mm[2] = v.z;

@@ -1,0 +1,75 @@
+"""Row-sharded protocol on one GPU: `world` logical ranks in one launch.
+
+Each row's tree stays on one rank, so the sharded trajectory must equal the
+pinned oracle (and the unsharded kernels) bit for bit.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import assert_bit_equal
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,world,fam", [(1000, 2, 0), (1000, 3, 0x1), (3001, 4, 0x1),
+                                         (10000, 2, 0), (257, 8, 0)])
+def test_logical_ranks_bit_exact(oracle_mod, n, world, fam):
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200.sharding import integrate_logical
+
+    g = np.random.default_rng(n + world)
+    w = g.uniform(-1, 1, (n, n)) / np.sqrt(n / 3.0)
+    np.fill_diagonal(w, 0.0)
+    top = sto.Topology(sto.CouplingMatrix(w), sto.InputWeights(g.uniform(-1, 1, (n, 1))))
+    steps = 3 if n >= 10000 else 40
+    stride = max(1, steps // 4)
+    samples = g.uniform(-1, 1, (steps, 1))
+    consts = sto.kernel_scalars(sto.PhysicalParams())
+    want, _ = oracle_mod.integrate(w, top.input_weights.entries, consts, sto.initial_state(n),
+                                   samples, 1, 1e-11, steps, stride)
+    m = sto.initial_state(n)
+    got = integrate_logical(top, sto.PhysicalParams(), m, samples, 1, 1e-11, steps, stride,
+                            world, flags=fam)
+    assert_bit_equal(got, want, f"n={n} world={world}")
+    assert_bit_equal(m, want[-1], "final m")
+
+
+def test_repeated_group_runs_reuse_epochs(oracle_mod):
+    """Epochs continue across launches (flags are never reset); two runs in a row."""
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200 import _native
+    from paper_2312_01121_b200.sharding import _shard_plan, shard_rows
+    import torch
+
+    n, world = 600, 2
+    top = sto.build_topology(n, seed=3)
+    consts = sto.kernel_scalars(sto.PhysicalParams())
+    plans = [_shard_plan(top, consts, b, c, world, r, 0) for r, (b, c) in enumerate(shard_rows(n, world))]
+    _native.connect_local(plans)
+    want, _ = oracle_mod.integrate(top.coupling.entries, top.input_weights.entries, consts,
+                                   sto.initial_state(n), np.zeros((1, 1)), 1, 1e-11, 30, 10)
+    for _ in range(2):
+        m = torch.as_tensor(sto.initial_state(n), device="cuda")
+        st = torch.empty((4, n, 3), dtype=torch.float64, device="cuda")
+        _native.integrate_group(plans, m, torch.zeros((1, 1), dtype=torch.float64, device="cuda"),
+                                1, 1e-11, 30, 10, st)
+        assert_bit_equal(st.cpu().numpy(), want)
+    for p in plans:
+        p.close()
+
+
+def test_group_divergence_is_consistent():
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200.sharding import integrate_logical
+
+    n = 1200
+    top = sto.Topology(sto.CouplingMatrix.zeros(n), sto.InputWeights(np.full((n, 1), 0.5)))
+    drive = np.zeros((20, 1))
+    drive[11:] = 1e12
+    with pytest.raises(sto.IntegrationDivergedError) as info:
+        integrate_logical(top, sto.PhysicalParams(), sto.initial_state(n), drive, 5, 1e-11, 100,
+                          10, world=3)
+    assert info.value.step == 60
