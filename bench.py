@@ -23,9 +23,10 @@ Arms
                   "port": the reference is pure Python/numba, nothing to
                   compile) on all host cores, bounded sample of the workload.
 
-Multi-GPU (torchrun): ranks run independent replicas of the workload
-(the row-sharded single trajectory is not wired into bench yet), so
-scaling is "weak".
+Multi-GPU (torchrun): n1e4 / n4e4 shard the ONE trajectory's rows over the
+ranks (peer-store all-gather of x inside the persistent kernel; "scaling":
+"strong"); ens512 shards members (no communication); n1 / n100 / n1000 run
+replicas ("weak").
 """
 
 from __future__ import annotations
@@ -55,6 +56,7 @@ WORKLOADS = {
                "1e4 RK4 steps, FP64 tensor-core (DMMA) coupling GEMM", False),
 }
 ENSEMBLE_BATCH = {"ens512": 512}
+SHARDED_WORKLOADS = ("n1e4", "n4e4")  # row-sharded over GPUs when --gpus > 1
 # FP64 peaks measured on this pool's B200 (tools/fp64_peak.cu; MEASURED_PEAKS.json has
 # none): DMMA m8n8k4 37.1 TFLOP/s, DFMA 34.0, cuBLAS DGEMM 8192^3 35.5.
 FP64_TENSOR_PEAK_TFLOPS = 37.1
@@ -73,9 +75,30 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "fallback": True}
 
 
+def synthetic_topology(n: int, seed: int = 0):
+    """N > 2e4: build_topology's Arnoldi would take ~20 min on the host (SURVEY
+    §7), so W is uniform[-1,1) off-diagonal scaled by sqrt(3/N) (circular law:
+    spectral radius ~1, the same normalisation in distribution)."""
+    import paper_2312_01121_b200 as sto
+
+    g = np.random.default_rng(seed)
+    w = np.empty((n, n))
+    for r0 in range(0, n, 4096):
+        blk = g.random((min(4096, n - r0), n))
+        blk *= 2.0
+        blk -= 1.0
+        blk *= np.sqrt(3.0 / n)
+        w[r0:r0 + blk.shape[0]] = blk
+    np.fill_diagonal(w, 0.0)
+    return sto.Topology(sto.CouplingMatrix(w), sto.InputWeights(g.uniform(-1, 1, (n, 1))))
+
+
 def cached_topology(n: int, seed: int = 0):
     """build_topology(n, seed) with a /dev/shm cache (same box, both arms)."""
     import paper_2312_01121_b200 as sto
+
+    if n > 20000:
+        return synthetic_topology(n, seed)
 
     cache = Path("/dev/shm") / f"sto_topology_n{n}_s{seed}.npz"
     if cache.exists():
@@ -376,8 +399,20 @@ def run_ours(args, rank, world, local_rank):
     samples = samples[:steps] if samples.shape[0] > 1 else samples
 
     # ------------------------------------------------------------ value ----
-    backend = B200Backend(top, params, device=dev)
-    info = backend.plan_info
+    # N > 1 GPUs: the single trajectory is row-sharded (NVLink all-gather of x
+    # inside the kernel) for the large-N workloads; small N runs replicas.
+    sharded = world > 1 and name in SHARDED_WORKLOADS
+    if sharded:
+        from paper_2312_01121_b200.sharding import ShardedB200Backend
+
+        backend = ShardedB200Backend(top, params, device=dev)
+        rows_mine = backend.shards[rank][1]
+        info = {"kernel_name": "stream-sharded", "grid": torch.cuda.get_device_properties(dev)
+                .multi_processor_count, "w_bytes": 8 * rows_mine * n}
+    else:
+        backend = B200Backend(top, params, device=dev)
+        info = backend.plan_info
+        rows_mine = n
     nrec = _native.n_records(steps, stride)
     m0 = torch.as_tensor(sto.initial_state(n), device="cuda")
     samples_d = torch.as_tensor(samples, device="cuda")
@@ -385,12 +420,12 @@ def run_ours(args, rank, world, local_rank):
     states_d = torch.empty((nrec, n, 3), dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
 
-    def one_run():
-        m_d.copy_(m0)
+    def launch():
         backend._plan.integrate_dev(m_d, samples_d, sps, DT, steps, stride, states_d, sync=False)
 
     for _ in range(args.warmup):
-        one_run()
+        m_d.copy_(m0)
+        launch()
     backend._plan.last_status()
     torch.cuda.synchronize()
     kstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -404,8 +439,7 @@ def run_ours(args, rank, world, local_rank):
         for i in range(args.steps):
             m_d.copy_(m0)
             kstart[i].record(stream)
-            backend._plan.integrate_dev(m_d, samples_d, sps, DT, steps, stride, states_d,
-                                        sync=False)
+            launch()
             kstop[i].record(stream)
         t_stop.record(stream)
         torch.cuda.synchronize()
@@ -416,7 +450,9 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([total_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_s = float(t.item())
-    value = world * n * steps * args.steps / total_s
+    # sharded: the whole job is ONE trajectory of n oscillators (strong scaling);
+    # replicas: every rank integrates its own copy (weak scaling)
+    value = (1 if sharded else world) * n * steps * args.steps / total_s
     launches = 2 * args.steps  # reset_status_kernel + persistent RK4 kernel per run
 
     # -------------------------------------------------------------- e2e ----
@@ -429,24 +465,34 @@ def run_ours(args, rank, world, local_rank):
     series = sto.InputSeries(samples, sps)
     cfg = sto.RunConfig(n=n, steps=steps, dt=DT, record_stride=stride, input_series=series,
                         backend="gpu", gpu_device=dev)
+
+    def e2e_once():
+        if sharded:
+            be = ShardedB200Backend(top_pinned, params, device=dev)  # W shard upload
+            try:
+                return sto.integrate(top_pinned, params, cfg, backend=be)
+            finally:
+                be.close()
+        return sto.integrate(top_pinned, params, cfg)
+
     e2e_steps = max(1, min(args.steps, 3))
-    sto.integrate(top_pinned, params, cfg)  # warm
+    e2e_once()  # warm
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        traj = sto.integrate(top_pinned, params, cfg)
+        traj = e2e_once()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if dist:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    h2d = 8 * (n * n + n * 1 + 3 * n + samples.size)
+    h2d = 8 * (rows_mine * n + n * 1 + 3 * n + samples.size)
     d2h = 8 * (traj.states.size + 3 * n)
 
     # -------------------------------------------------------- roofline ----
     peaks = measured_peaks()
-    alg_bytes = 32.0 * n * n * steps  # one f64 W row per RK stage per oscillator-step
+    alg_bytes = 32.0 * rows_mine * n * steps  # one f64 W row per RK stage per (own) osc-step
     achieved = alg_bytes / kernel_s / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
@@ -470,16 +516,18 @@ def run_ours(args, rank, world, local_rank):
             "metric": "oscillator-steps/s", "value": value, "unit": "osc-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_s * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (build_topology(n, seed=0), u=0 / seeded uniform drive)",
             "config": {"workload": desc, "n": n, "rk4_steps_per_run": steps,
                        "record_stride": stride, "dt": DT,
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"row-sharded x{world} (in-kernel NVLink all-gather)"
+                                       if sharded else f"replicas x{world}" if world > 1
+                                       else "1 GPU"),
                        "kernel": info["kernel_name"], "grid": info["grid"],
                        "l2": ("inputs larger than L2 (W %.0f MB)" % (info["w_bytes"] / 1e6))
                        if info["w_bytes"] > 126e6 else
                        "W on-chip/L2-resident by design (persistent kernel; one launch per run)"},
-            "e2e": {"value": world * n * steps / e2e_s, "unit": "osc-steps/s",
+            "e2e": {"value": (1 if sharded else world) * n * steps / e2e_s, "unit": "osc-steps/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": roofline,

@@ -352,14 +352,17 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
             }
         }
         if (!integrate) break;
-        if (e + 1 == total_stages) break;
+        // MULTI also synchronises after the last stage, so that no rank can start
+        // its next run (and write into a peer's buffer) while a peer still reads
+        if (e + 1 == total_stages && !MULTI) break;
         // ---------------- exchange of the stage x-vector ----------------
         if constexpr (SINGLE) {
             __syncthreads();
             if (*sflag) break;
         } else if constexpr (MULTI) {
             if (multi_sync(p.mp, sh, rank, b, (unsigned long long)(e + 1) * G,
-                           p.mp.epoch_base + e + 1, stage == 3 && rec >= 0, p.status, sflag))
+                           p.mp.epoch_base + e + 1, stage == 3 && rec >= 0, p.status, sflag) ||
+                e + 1 == total_stages)
                 break;
         } else {
             grid_sync(p.bar, (unsigned long long)(e + 1) * G);
