@@ -173,6 +173,7 @@ struct sto_plan {
     size_t smem = 0;
     int threads = 512;
     int team = 0;  // kReg: threads per row
+    int rows_per_team = 1;
     // row sharding (world > 1)
     int world = 1, rank = 0;
     long long row_begin = 0;
@@ -243,9 +244,9 @@ ShardInfo shard_info(const sto_plan *P) {
     return s;
 }
 
-template <int T, int C, bool SINGLE>
+template <int T, int C, int R, bool SINGLE>
 int launch_reg_t(const RegParams &rp, int grid, int threads, size_t smem, cudaStream_t stream) {
-    auto fn = reg_rk4_kernel<T, C, SINGLE>;
+    auto fn = reg_rk4_kernel<T, C, R, SINGLE>;
     STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (SINGLE) {
         fn<<<1, threads, smem, stream>>>(rp);
@@ -258,25 +259,27 @@ int launch_reg_t(const RegParams &rp, int grid, int threads, size_t smem, cudaSt
     return STO_OK;
 }
 
-// (team T, columns per thread C): n <= 128 uses C = 32 in one CTA; larger n
-// uses C = 16 over the grid.  P = T * C is the padded row width.
-int launch_reg(const RegParams &rp, int team, int cols, bool single, int grid, int threads,
-               size_t smem, cudaStream_t s) {
+// (team T, columns per thread C, rows per team R): n <= 128 uses C = 32 in
+// one CTA; larger n uses C = 16 over the grid, R = 2 rows per team for the
+// 64-thread teams (each shared-memory x load then feeds two rows).
+int launch_reg(const RegParams &rp, int team, int rows_per_team, bool single, int grid,
+               int threads, size_t smem, cudaStream_t s) {
     if (single) {
         switch (team) {
-            case 1: return launch_reg_t<1, 32, true>(rp, grid, threads, smem, s);
-            case 2: return launch_reg_t<2, 32, true>(rp, grid, threads, smem, s);
-            default: return launch_reg_t<4, 32, true>(rp, grid, threads, smem, s);
+            case 1: return launch_reg_t<1, 32, 1, true>(rp, grid, threads, smem, s);
+            case 2: return launch_reg_t<2, 32, 1, true>(rp, grid, threads, smem, s);
+            default: return launch_reg_t<4, 32, 1, true>(rp, grid, threads, smem, s);
         }
     }
-    (void)cols;
     switch (team) {
-        case 2: return launch_reg_t<2, 16, false>(rp, grid, threads, smem, s);
-        case 4: return launch_reg_t<4, 16, false>(rp, grid, threads, smem, s);
-        case 8: return launch_reg_t<8, 16, false>(rp, grid, threads, smem, s);
-        case 16: return launch_reg_t<16, 16, false>(rp, grid, threads, smem, s);
-        case 32: return launch_reg_t<32, 16, false>(rp, grid, threads, smem, s);
-        default: return launch_reg_t<64, 16, false>(rp, grid, threads, smem, s);
+        case 2: return launch_reg_t<2, 16, 1, false>(rp, grid, threads, smem, s);
+        case 4: return launch_reg_t<4, 16, 1, false>(rp, grid, threads, smem, s);
+        case 8: return launch_reg_t<8, 16, 1, false>(rp, grid, threads, smem, s);
+        case 16: return launch_reg_t<16, 16, 1, false>(rp, grid, threads, smem, s);
+        case 32: return launch_reg_t<32, 16, 1, false>(rp, grid, threads, smem, s);
+        default:
+            return rows_per_team == 2 ? launch_reg_t<64, 16, 2, false>(rp, grid, threads, smem, s)
+                                      : launch_reg_t<64, 16, 1, false>(rp, grid, threads, smem, s);
     }
 }
 
@@ -445,9 +448,16 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         }
         P->grid = g;
         P->rows_cap = (n + g - 1) / g;
-        P->threads = ((P->rows_cap * team + 31) / 32) * 32;  // >= rows_cap (RHS owners)
+        P->rows_per_team = (!single && team == 64 && !getenv("STO_REG_R1")) ? 2 : 1;
+        int teams = (P->rows_cap + P->rows_per_team - 1) / P->rows_per_team;
+        if (P->rows_per_team == 2 && teams * team > 256) {  // R = 2 kernel is built for 256 threads
+            P->rows_per_team = 1;
+            teams = P->rows_cap;
+        }
+        P->threads = std::max(((teams * team + 31) / 32) * 32, ((P->rows_cap + 31) / 32) * 32);
         P->chunk_cols = single ? 1 : 0;  // marks SINGLE for the launcher
-        P->smem = sizeof(double) * ((size_t)team * cols + 2 * (size_t)(P->threads / team) + 8);
+        P->smem = sizeof(double) * ((size_t)team * cols + 2 * (size_t)P->rows_per_team *
+                                    (P->threads / team) + 8);
         if (P->threads > 512 || g > kMaxFlags)
             return bail(fail(STO_E_PARAM, "register-resident kernel does not fit"));
     } else if ((fl & STO_PLAN_FORCE_SINGLE) ||
@@ -585,7 +595,8 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
         case kReg: {
             RegParams rp{p, P->ll};
             STO_CUDA(cudaMemsetAsync(P->ll, 0, sizeof(uint4) * 2 * (size_t)P->n, s));
-            rc = launch_reg(rp, P->team, 0, P->chunk_cols == 1, P->grid, P->threads, P->smem, s);
+            rc = launch_reg(rp, P->team, P->rows_per_team, P->chunk_cols == 1, P->grid, P->threads,
+                            P->smem, s);
             break;
         }
         case kSingle: rc = launch_grid<WSrc::Shared, true>(p, 1, P->smem, false, s); break;

@@ -36,32 +36,49 @@ struct V3 {
 
 // dm/dt of one oscillator given its coupling row sum `cp` and input row sum
 // `cin`.  cpu_jit.py:62-87 / model.py:239-301, operation for operation.
-__device__ __forceinline__ V3 row_rhs(V3 m, double cp, double cin, const Consts &c) {
+// Split in two: everything that depends only on the oscillator's own state
+// (row_rhs_pre: m.p, the IEEE division for h_s, p x m, b_y, b_z, (m x b)_x)
+// can be evaluated while the coupling GEMV / exchange is still in flight;
+// row_rhs_post finishes once cp is known.  Same operations, same order.
+struct RhsPre {
+    V3 m;
+    double hs_qx, by, bz, ax, ain_cin;
+};
+
+__device__ __forceinline__ RhsPre row_rhs_pre(V3 m, double cin, const Consts &c) {
     double md = radd(rmul(m.x, c.px), rmul(m.y, c.py));
     md = radd(md, rmul(m.z, c.pz));
     const double hs = rdiv(c.pref, radd(1.0, rmul(c.lam, md)));
-
     const double qx = rsub(rmul(c.py, m.z), rmul(c.pz, m.y));
     const double qy = rsub(rmul(c.pz, m.x), rmul(c.px, m.z));
     const double qz = rsub(rmul(c.px, m.y), rmul(c.py, m.x));
+    RhsPre r;
+    r.m = m;
+    r.hs_qx = rmul(hs, qx);
+    r.by = rmul(hs, qy);
+    r.bz = radd(radd(c.h_appl, rmul(c.h_aniso, m.z)), rmul(hs, qz));
+    r.ax = rsub(rmul(m.y, r.bz), rmul(m.z, r.by));
+    r.ain_cin = rmul(c.a_in, cin);
+    return r;
+}
 
-    const double bx = radd(radd(rmul(c.a_cp, cp), rmul(c.a_in, cin)), rmul(hs, qx));
-    const double by = rmul(hs, qy);
-    const double bz = radd(radd(c.h_appl, rmul(c.h_aniso, m.z)), rmul(hs, qz));
-
-    const double ax = rsub(rmul(m.y, bz), rmul(m.z, by));
-    const double ay = rsub(rmul(m.z, bx), rmul(m.x, bz));
-    const double az = rsub(rmul(m.x, by), rmul(m.y, bx));
-
+__device__ __forceinline__ V3 row_rhs_post(const RhsPre &r, double cp, const Consts &c) {
+    const V3 &m = r.m;
+    const double bx = radd(radd(rmul(c.a_cp, cp), r.ain_cin), r.hs_qx);
+    const double ay = rsub(rmul(m.z, bx), rmul(m.x, r.bz));
+    const double az = rsub(rmul(m.x, r.by), rmul(m.y, bx));
     const double ex = rsub(rmul(m.y, az), rmul(m.z, ay));
-    const double ey = rsub(rmul(m.z, ax), rmul(m.x, az));
-    const double ez = rsub(rmul(m.x, ay), rmul(m.y, ax));
-
+    const double ey = rsub(rmul(m.z, r.ax), rmul(m.x, az));
+    const double ez = rsub(rmul(m.x, ay), rmul(m.y, r.ax));
     V3 d;
-    d.x = rsub(-rmul(c.c_prec, ax), rmul(c.c_damp, ex));
+    d.x = rsub(-rmul(c.c_prec, r.ax), rmul(c.c_damp, ex));
     d.y = rsub(-rmul(c.c_prec, ay), rmul(c.c_damp, ey));
     d.z = rsub(-rmul(c.c_prec, az), rmul(c.c_damp, ez));
     return d;
+}
+
+__device__ __forceinline__ V3 row_rhs(V3 m, double cp, double cin, const Consts &c) {
+    return row_rhs_post(row_rhs_pre(m, cin, c), cp, c);
 }
 
 // s = m + k*h   (integrator.py:107-108, 110-111, 113-114)

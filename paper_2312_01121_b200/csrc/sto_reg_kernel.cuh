@@ -78,42 +78,46 @@ __device__ __forceinline__ void tl_mark(long long e, int ev) {
 #define TL(e, ev)
 #endif
 
-template <int T, int C, bool SINGLE>
-__global__ void __launch_bounds__(512, 1) reg_rk4_kernel(const __grid_constant__ RegParams rp) {
+template <int T, int C, int R, bool SINGLE>
+__global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __grid_constant__ RegParams rp) {
     constexpr int P = T * C;
     constexpr int LV = (C == 32) ? 5 : 4;  // tree levels above the products
     const KParams &p = rp.k;
     extern __shared__ __align__(16) double smem[];
     const int teams = blockDim.x / T;
     double *xs = smem;                       // P doubles, team-blocked
-    double *cps = xs + P;                    // [teams][2] row sums (two warp halves if T = 64)
-    volatile int *sstop = reinterpret_cast<volatile int *>(cps + 2 * teams);
+    double *cps = xs + P;                    // [teams * R][2] row sums (two warp halves if T = 64)
+    volatile int *sstop = reinterpret_cast<volatile int *>(cps + 2 * R * teams);
 
     const int G = gridDim.x, b = blockIdx.x;
     const int n = p.rows;
     const int r0 = row_lo(b, G, n), nrow = row_lo(b + 1, G, n) - r0;
-    // GEMV role: team `team`, member j -- columns [C*j, C*j + C) of row r0 + team
+    // GEMV role: team `team`, member j -- columns [C*j, C*j + C) of rows
+    // r0 + R*team + i (i < R): every x value loaded from shared memory feeds R rows
     const int team = threadIdx.x / T, j = threadIdx.x % T;
-    const bool active = team < nrow;
     // RHS role: thread r < nrow owns oscillator r0 + r for the whole run, its
     // RK state lives in registers and the RHS work is packed into few warps
     const int r = threadIdx.x;
     const bool owner = r < nrow;
     const int k = r0 + r;
 
-    double w[C];
+    double w[R][C];
 #pragma unroll
-    for (int q = 0; q < C; ++q) {
-        const int col = j * C + q;
-        w[q] = (active && col < n) ? p.w[(size_t)(r0 + team) * p.cs.ldw + col_perm(p.cs, col)]
-                                   : -0.0;
+    for (int i = 0; i < R; ++i) {
+        const int row = R * team + i;
+#pragma unroll
+        for (int q = 0; q < C; ++q) {
+            const int col = j * C + q;
+            w[i][q] = (row < nrow && col < n)
+                          ? p.w[(size_t)(r0 + row) * p.cs.ldw + col_perm(p.cs, col)]
+                          : -0.0;
+        }
     }
     for (int i = threadIdx.x; i < P; i += blockDim.x) xs[i] = 0.0;
     __syncthreads();
     for (int col = threadIdx.x; col < n; col += blockDim.x)
         xs[reg_xpos<C>(col, T)] = p.m[3 * (size_t)col];
     V3 m{0.0, 0.0, 0.0}, s{0.0, 0.0, 0.0}, acc{0.0, 0.0, 0.0}, k3{0.0, 0.0, 0.0};
-    double cin = 0.0;
     if (owner) {
         m = V3{p.m[3 * (size_t)k], p.m[3 * (size_t)k + 1], p.m[3 * (size_t)k + 2]};
         if (p.states) {
@@ -131,10 +135,14 @@ __global__ void __launch_bounds__(512, 1) reg_rk4_kernel(const __grid_constant__
     long long rec_idx = 1;
     unsigned epoch = 0;
     bool stop = false;
+    RhsPre pre{};
     for (long long step = 1; step <= p.steps && !stop; ++step) {
-        if (owner)
+        double cin = 0.0;
+        if (owner) {
             cin = (p.n_in == 1) ? rmul(p.w_in[k], u[0])
                                 : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
+            if (!SINGLE) pre = row_rhs_pre(m, cin, p.c);  // own-state half for stage 0
+        }
         const bool record = (step == next_rec) || (step == p.steps);
 #pragma unroll 1
         for (int stage = 0; stage < 4; ++stage) {
@@ -143,35 +151,45 @@ __global__ void __launch_bounds__(512, 1) reg_rk4_kernel(const __grid_constant__
             // -------- team GEMV: pinned tree of w . x ----------------------
             // products streamed pair by pair through an unrolled binary
             // counter: completed siblings merge at once (<= log2(C) live nodes)
-            double lvl[LV];
+            double lvl[R][LV];
 #pragma unroll
             for (int i = 0; i < C / 2; ++i) {
                 const double2 x2 = *reinterpret_cast<const double2 *>(xs + ((i * T + j) << 1));
-                double node = radd(rmul(w[2 * i], x2.x), rmul(w[2 * i + 1], x2.y));
 #pragma unroll
-                for (int l = 0; l < LV - 1; ++l) {
-                    if (i & (1 << l)) node = radd(lvl[l], node);
-                    else { lvl[l] = node; break; }
+                for (int rr = 0; rr < R; ++rr) {
+                    double node = radd(rmul(w[rr][2 * i], x2.x), rmul(w[rr][2 * i + 1], x2.y));
+#pragma unroll
+                    for (int l = 0; l < LV - 1; ++l) {
+                        if (i & (1 << l)) node = radd(lvl[rr][l], node);
+                        else { lvl[rr][l] = node; break; }
+                    }
+                    if (i == C / 2 - 1) lvl[rr][LV - 1] = node;
                 }
-                if (i == C / 2 - 1) lvl[LV - 1] = node;
             }
-            double v = lvl[LV - 1];
 #pragma unroll
-            for (int mask = 1; mask < (T < 32 ? T : 32); mask <<= 1)
-                v = radd(v, __shfl_xor_sync(0xffffffffu, v, mask));
-            if (T == 64) {
-                if ((threadIdx.x & 31) == 0) cps[2 * team + ((threadIdx.x >> 5) & 1)] = v;
-            } else if (j == 0) {
-                cps[2 * team] = v;
+            for (int rr = 0; rr < R; ++rr) {
+                double v = lvl[rr][LV - 1];
+#pragma unroll
+                for (int mask = 1; mask < (T < 32 ? T : 32); mask <<= 1)
+                    v = radd(v, __shfl_xor_sync(0xffffffffu, v, mask));
+                const int row = R * team + rr;
+                if (T == 64) {
+                    if ((threadIdx.x & 31) == 0) cps[2 * row + ((threadIdx.x >> 5) & 1)] = v;
+                } else if (j == 0) {
+                    cps[2 * row] = v;
+                }
             }
             __syncthreads();  // every read of xs done; row sums in cps
             TL(estage, 1);
-            // -------- owners: RHS + RK4 stage update ------------------------
+            // -------- owners: cp-dependent half of the RHS + RK4 update -----
             double xpub = 0.0;
             bool bad = false;
             if (owner) {
                 const double cp = (T == 64) ? radd(cps[2 * r], cps[2 * r + 1]) : cps[2 * r];
-                const V3 d = row_rhs(stage == 0 ? m : s, cp, cin, p.c);
+                // grid: own-state half was computed during the exchange; single
+                // CTA (no exchange to hide behind): the whole RHS here
+                const V3 d = SINGLE ? row_rhs(stage == 0 ? m : s, cp, cin, p.c)
+                                    : row_rhs_post(pre, cp, p.c);
                 if (stage == 0) {
                     acc = d;
                     s = stage_point(m, d, p.h2);
@@ -209,9 +227,13 @@ __global__ void __launch_bounds__(512, 1) reg_rk4_kernel(const __grid_constant__
                 if (*sstop) stop = true;
             } else {
                 ++epoch;
-                if (owner)
+                if (owner) {
                     st_ll(rp.ll + (size_t)(epoch & 1) * n + k, xpub,
                           epoch | (bad ? 0x80000000u : 0u));
+                    // next stage's own-state half, off the critical path: the
+                    // exchange below takes an L2 round trip anyway
+                    if (stage < 3) pre = row_rhs_pre(s, cin, p.c);
+                }
                 TL(estage, 2);
                 if (!last) {
                     const uint4 *slot = rp.ll + (size_t)(epoch & 1) * n;
