@@ -105,13 +105,21 @@ __global__ void permute_rows_kernel(const double *__restrict__ src, long long ld
 constexpr int kMaxFlags = 1024;
 
 // logical row-major (zero padded to np x np) copy of W from the device layout
-__global__ void unpermute_rows_kernel(const double *__restrict__ src, double *__restrict__ dst,
-                                      int rows, int np, int kp, ColSched cs) {
-    const long long total = (long long)np * kp;
+// Ensemble W in DMMA fragment order for row tiles of TR = 8U rows
+// (sto_ensemble_kernel.cuh, ens layout comment); zero outside n x n.
+__global__ void ens_layout_kernel(const double *__restrict__ src, double *__restrict__ dst, int n,
+                                  int kp, int tr, int n_rt, ColSched cs) {
+    const long long tile = (long long)tr * kp, total = tile * n_rt;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(i / kp), c = (int)(i - (long long)r * kp);
-        dst[i] = (r < rows && c < cs.n) ? src[(long long)r * cs.ldw + col_perm(cs, c)] : 0.0;
+        const int rt = (int)(i / tile);
+        const int rem = (int)(i - (long long)rt * tile);
+        const int ch = rem / (tr * kEnsKC);
+        const int within = rem - ch * tr * kEnsKC;
+        const int nk = min(kEnsKC, kp - ch * kEnsKC) >> 2;
+        const int ru = within / (nk * 32), ks = (within / 32) % nk, lane = within & 31;
+        const int row = rt * tr + 8 * ru + (lane >> 2), col = ch * kEnsKC + 4 * ks + (lane & 3);
+        dst[i] = (row < n && col < n) ? src[(long long)row * cs.ldw + col_perm(cs, col)] : 0.0;
     }
 }
 
@@ -188,6 +196,7 @@ struct sto_plan {
     // ensemble resources (allocated on first sto_integrate_ensemble)
     double *ens_w = nullptr;           // np x np row-major, zero padded
     int ens_np = 0;
+    int ens_u = 0;                     // tile height ens_w is laid out for
     double *ens_x = nullptr, *ens_st = nullptr;
     size_t ens_bp = 0;                 // member capacity of ens_x / ens_st
     unsigned long long *ens_bar = nullptr;
@@ -611,6 +620,34 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
     return STO_OK;
 }
 
+}  // extern "C"
+
+namespace {
+template <int U>
+int launch_ens(const EnsParams &e, int grid, cudaStream_t s) {
+    const size_t smem = ens_smem_bytes(U);
+    STO_CUDA(cudaFuncSetAttribute(ens_rk4_kernel<U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    void *args[] = {(void *)&e};
+    STO_CUDA(cudaLaunchCooperativeKernel((void *)ens_rk4_kernel<U>, dim3(grid), dim3(kEnsThreads),
+                                         args, smem, s));
+    return STO_OK;
+}
+int launch_ens_u(int u, const EnsParams &e, int grid, cudaStream_t s) {
+    switch (u) {
+        case 1: return launch_ens<1>(e, grid, s);
+        case 2: return launch_ens<2>(e, grid, s);
+        case 3: return launch_ens<3>(e, grid, s);
+        case 4: return launch_ens<4>(e, grid, s);
+        case 5: return launch_ens<5>(e, grid, s);
+        case 6: return launch_ens<6>(e, grid, s);
+        default: return launch_ens<7>(e, grid, s);
+    }
+}
+}  // namespace
+
+extern "C" {
+
 int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *status,
                            void *stream) {
     if (!P || !r) return fail(STO_E_PARAM, "null plan or run");
@@ -620,40 +657,65 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
         return fail(STO_E_PARAM, "bad ensemble run descriptor");
     STO_CUDA(cudaSetDevice(P->device));
     cudaStream_t s = (cudaStream_t)stream;
-    const int np = ((P->n + kEnsRT - 1) / kEnsRT) * kEnsRT;
-    const int kp = ((P->n + kEnsKC - 1) / kEnsKC) * kEnsKC;
-    const int n_rt = np / kEnsRT;
-    const int max_cols = std::max(1, P->sm_count / n_rt);
-    if (n_rt > P->sm_count) return fail(STO_E_PARAM, "ensemble needs n <= 64 * SM count");
+    // Tile choice: TR = 8U rows x 64 members per CTA.  Minimise the per-SM
+    // work U * (number of launches) over U = 1..8 (ties -> larger U: fewer
+    // row tiles re-reading X).
+    const int nu = (P->n + 7) / 8;  // 8-row units
     const int total_cols = (int)((r->batch + kEnsBT - 1) / kEnsBT);
-    const int cols_per_launch = std::min(max_cols, total_cols);
+    int best_u = 0, best_launch_cols = 0;
+    long long best_cost = 0;
+    for (int u = 1; u <= kEnsMaxU; ++u) {
+        const int n_rt = (nu + u - 1) / u;
+        if (n_rt > P->sm_count) continue;
+        const int cols = std::min(total_cols, P->sm_count / n_rt);
+        const long long cost = (long long)u * ((total_cols + cols - 1) / cols);
+        if (!best_u || cost <= best_cost) {
+            best_u = u;
+            best_cost = cost;
+            best_launch_cols = cols;
+        }
+    }
+    if (!best_u) return fail(STO_E_PARAM, "ensemble needs n <= 64 * SM count");
+    if (const char *ev = getenv("STO_ENS_U")) {  // tuning override
+        const int u = atoi(ev);
+        if (u >= 1 && u <= kEnsMaxU && (nu + u - 1) / u <= P->sm_count) {
+            best_u = u;
+            best_launch_cols = std::min(total_cols, P->sm_count / ((nu + u - 1) / u));
+        }
+    }
+    const int U = best_u, TR = 8 * U;
+    const int n_rt = (nu + U - 1) / U;
+    const int cols_per_launch = best_launch_cols;
+    const int kp = ((P->n + kEnsKAlign - 1) / kEnsKAlign) * kEnsKAlign;
+    const int np_alloc = nu * 8 + 8 * kEnsMaxU;  // any n_rt * TR fits
     const size_t bp = (size_t)cols_per_launch * kEnsBT;
     if (!P->ens_w) {
-        STO_CUDA(cudaMalloc(&P->ens_w, sizeof(double) * (size_t)np * kp));
-        unpermute_rows_kernel<<<1184, 256, 0, s>>>(P->L.w, P->ens_w, P->n, np, kp, P->L.cs);
-        STO_CUDA(cudaGetLastError());
-        P->ens_np = np;
+        STO_CUDA(cudaMalloc(&P->ens_w, sizeof(double) * (size_t)np_alloc * kp));
+        P->ens_np = np_alloc;
         STO_CUDA(cudaMalloc(&P->ens_bar, sizeof(unsigned long long) * 32 * 1024));
+    }
+    if (P->ens_u != U) {  // W in fragment order for this tile height
+        ens_layout_kernel<<<1184, 256, 0, s>>>(P->L.w, P->ens_w, P->n, kp, TR, n_rt, P->L.cs);
+        STO_CUDA(cudaGetLastError());
+        P->ens_u = U;
     }
     if (P->ens_bp < bp) {
         cudaFree(P->ens_x);
         cudaFree(P->ens_st);
         P->ens_x = P->ens_st = nullptr;
-        STO_CUDA(cudaMalloc(&P->ens_x, sizeof(double) * 2 * std::max(np, kp) * bp));
-        STO_CUDA(cudaMalloc(&P->ens_st, sizeof(double) * kEnsState * np * bp));
+        STO_CUDA(cudaMalloc(&P->ens_x, sizeof(double) * 2 * kp * bp));
+        STO_CUDA(cudaMalloc(&P->ens_st, sizeof(double) * kEnsState * np_alloc * bp));
         P->ens_bp = bp;
     }
-    const size_t smem = sizeof(double) * kEnsSmemDoubles;
-    STO_CUDA(cudaFuncSetAttribute(ens_rk4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
     reset_status_kernel<<<1, 256, 0, s>>>(P->status, P->bar, P->flags);
     STO_CUDA(cudaGetLastError());
     for (int c0 = 0; c0 < total_cols; c0 += cols_per_launch) {
         const int ncols = std::min(cols_per_launch, total_cols - c0);
         EnsParams e{};
         e.n = P->n;
-        e.np = np;
+        e.np = np_alloc;
         e.kp = kp;
+        e.n_rt = n_rt;
         e.batch = (int)r->batch;
         e.bp = (int)bp;
         e.member0 = c0 * kEnsBT;
@@ -677,11 +739,11 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
         e.st = P->ens_st;
         e.bar = P->ens_bar;
         e.status = P->status;
-        STO_CUDA(cudaMemsetAsync(P->ens_x, 0, sizeof(double) * 2 * std::max(np, kp) * bp, s));
+        e.debug_solo = getenv("STO_ENS_DEBUG_SOLO") ? 1 : 0;
+        STO_CUDA(cudaMemsetAsync(P->ens_x, 0, sizeof(double) * 2 * kp * bp, s));
         STO_CUDA(cudaMemsetAsync(P->ens_bar, 0, sizeof(unsigned long long) * 32 * 1024, s));
-        void *args[] = {(void *)&e};
-        STO_CUDA(cudaLaunchCooperativeKernel((void *)ens_rk4_kernel, dim3(n_rt * ncols),
-                                             dim3(kEnsThreads), args, smem, s));
+        const int rc = launch_ens_u(U, e, n_rt * ncols, s);
+        if (rc) return rc;
     }
     if (!status) return STO_OK;
     StatusDev h{};

@@ -1,7 +1,8 @@
 // sto_ensemble_kernel.cuh -- batched ensemble (BASELINE configs[3]): B
 // independent reservoirs that share W and W_in but not their parameters
 // (e.g. a sweep over the drive current), stepped together so the coupling
-// becomes a GEMM:  CP[k][b] = sum_j W[k][j] * X[j][b]   (X = member x-vectors).
+// becomes a GEMM per RK stage:  CP[k][b] = sum_j W[k][j] * X[j][b]
+// (X = the members' stage x-vectors).
 //
 // The GEMM runs on the FP64 tensor cores: mma.sync.aligned.m8n8k4 .f64
 // (SASS DMMA.8x8x4 -- sm_100 has no tcgen05 f64 kind; DMMA is its fp64
@@ -10,41 +11,96 @@
 // held to a tolerance (<= 1e-10 at 1e3 steps, per member,
 // against the oracle run with that member's parameters), not bit-equality.
 //
-// Tiling: one CTA per 64-row x 64-member output tile (N = 1000, B = 512 ->
-// 16 x 8 = 128 CTAs); 16 warps, each a 16 x 16 region = 2 x 2 DMMA tiles fed
-// by 2 A + 2 B fragments per k-step (256 B of shared-memory operand traffic
-// per DMMA; 8 warps of 16 x 32 tiles measured slower: too little latency
-// hiding for the DMMA chains); K streamed
-// in 64-column chunks through a 3-stage cp.async pipeline (68-double padded
-// rows: conflict-free fragment loads).  The RK4 epilogue re-maps the
-// accumulators through shared memory so that consecutive threads own
-// consecutive members: the per-(row, member) RK state (m, s, acc, k3, cin),
-// kept in L2-resident global SoA arrays, is then read and written with
-// coalesced, batched loads.  Members of different 64-member
-// columns never interact, so the per-stage exchange is a barrier among the
-// CTAs of one column only.
+// Structure (one persistent cooperative launch per run):
+//  * Tiles: CTA = TR = 8U rows x 64 members, U chosen on the host so that
+//    ceil(n/TR) row tiles x ceil(B/64) member columns fill the 148 SMs
+//    (N = 1000, B = 512: U = 7 -> 18 x 8 = 144 CTAs, 96.5 % of the ideal
+//    per-SM share; 64-row tiles would leave 20 SMs idle).
+//  * Two independent warp groups per CTA (8 warps each), one per 32-member
+//    half of the column.  Each group runs its own K-loop ring, exchange
+//    counter and epilogue; the halves never interact.  Group 1 starts half a
+//    GEMM after group 0, so while one group is in its epilogue (FP64 pipe,
+//    tensor memory) and exchange wait, the other keeps the DMMA pipe busy:
+//    per-stage time -> the two GEMMs back to back instead of GEMM + epilogue
+//    + exchange (any start offset between the epilogue length and GEMM
+//    length is a stable operating point -- tools/ens_overlap_model.py).
+//  * Fragment-order operands: W (a private copy, re-laid out per tile
+//    height) and the stage X (written so by the epilogue) are stored in HBM
+//    in DMMA fragment order -- for each (8-row unit, k-step) / (k-step,
+//    8-member unit) the 32 doubles of one fragment in lane order -- so that
+//    the W part and the X part of one (tile, K chunk) are each ONE
+//    contiguous block (14 KB + 8 KB at U = 7), moved by ONE 1-D bulk async
+//    copy (cp.async.bulk ... mbarrier::complete_tx), and every fragment load
+//    is a conflict-free 256 B warp-contiguous LDS.64.  K streams in
+//    32-column chunks through a 4-slot ring per group with one "full"
+//    mbarrier per slot.  There is no producer warp (a 17th warp would cap
+//    every thread at 96 registers: 5 warps on one SM sub-partition): the
+//    LAST of the group's warps to finish a chunk (shared-memory counter)
+//    refills its slot, so no warp ever waits to issue.  W does not depend on
+//    the stage, so the slots of the first chunks of stage e+1 are refilled
+//    with W while stage e's last chunks and epilogue still run; their X
+//    parts are issued once the half-column's exchange counter shows every
+//    row tile has published x.
+//  * GEMM warps: warp w of group h owns member unit w&3 of the half and
+//    k-steps of parity (w>>2)&1 (intra-group split-K 2), i.e. a U x 1 grid
+//    of 8x8 DMMA tiles fed by U A-fragments + 1 B-fragment per k-step.
+//    Partials are summed through shared memory.
+//  * Epilogue: every thread owns U outputs (one member, rows 8j + 4((w>>2)&1)
+//    + lane%4) -- so each warp's x publication is 32 consecutive doubles of
+//    the fragment-order X (one 256 B store).  The RK state of every output
+//    (m, the running RK4 accumulator, the stage point: 9 doubles) lives in
+//    TENSOR MEMORY -- the 256 KB TMEM is otherwise idle (fp64 has no
+//    tcgen05 MMA kind) and holds 7 outputs x 18 columns in each thread's
+//    128-column slice of its lane (tcgen05.ld/st 32x32b).  Kept in L2
+//    instead, the state round trip made the epilogue L2-bandwidth bound
+//    (~56 MB per stage).
+//  * RK4 combination: acc = (k1 + k2*2) + k3*2 and m + (acc + k4)*dt/6, a
+//    reassociation of the reference's m + ((k1 + k2*2) + (k3*2 + k4))*dt/6
+//    (1 ulp level, inside the GEMM-order tolerance) that drops k3 from the
+//    live state.
+//  * Exchange: one counter per half-column (red.release.gpu by each CTA's
+//    group after its epilogue; acquire-polled by one thread of the group,
+//    which then issues the X copies -- everybody else waits on shared-memory
+//    mbarriers).
 #pragma once
 
 #include "sto_kernels.cuh"
 
 namespace sto {
 
-constexpr int kEnsRT = 64;      // rows per CTA tile
-constexpr int kEnsBT = 64;      // members per CTA tile
-constexpr int kEnsKC = 64;      // K chunk
-constexpr int kEnsLD = kEnsKC + 4;  // padded smem row (doubles)
-constexpr int kEnsThreads = 512;    // 16 warps = 4 row groups (16) x 4 member quarters (16)
-constexpr int kEnsState = 13;       // m, s, acc, k3 (3 each) + cin
-constexpr int kEnsStages = 3;       // cp.async pipeline depth
-constexpr int kEnsBuf = (kEnsRT + kEnsKC) * kEnsLD;  // one stage: W tile + X tile
-constexpr int kEnsSmemDoubles = kEnsStages * kEnsBuf + kEnsBT * 11;
+constexpr int kEnsBT = 64;                      // members per CTA tile
+constexpr int kEnsGW = 32;                      // members per warp group (half-column)
+constexpr int kEnsGroups = kEnsBT / kEnsGW;
+constexpr int kEnsKC = 32;                      // K chunk (doubles)
+constexpr int kEnsLDB = kEnsBT + 4;             // CP (coupling sums) row pitch
+constexpr int kEnsSlots = 4;                    // shared-memory ring depth per group
+constexpr int kEnsThreads = 512;                // 2 groups x 8 MMA + epilogue warps
+constexpr int kEnsGroupThreads = kEnsThreads / kEnsGroups;
+constexpr int kEnsMaxU = 7;                     // TR <= 56 rows (RK state of 7 outputs fills a TMEM lane slice)
+constexpr int kEnsState = 1;                    // global state planes: cin (n_in > 1 only)
+constexpr int kEnsTmemCols = 512;               // whole TMEM: 128 lanes x 512 x 32 bit
+#ifndef STO_ENS_EPI_UNROLL
+#define STO_ENS_EPI_UNROLL 2
+#endif
+constexpr int kEnsEpiUnroll = STO_ENS_EPI_UNROLL;  // epilogue outputs in flight per thread
+constexpr int kEnsTmemOut = 18;                 // columns per output: m, acc, s (3 doubles each)
+constexpr int kEnsKAlign = 8;                   // K padded to 8: chunk bytes % 16 == 0, even k-steps
+
+__host__ __device__ constexpr int ens_slot_doubles(int u) { return 8 * u * kEnsKC + kEnsKC * kEnsGW; }
+__host__ __device__ constexpr size_t ens_smem_bytes(int u) {
+    return sizeof(double) * ((size_t)kEnsGroups * kEnsSlots * ens_slot_doubles(u) + 8 * u * kEnsLDB +
+                             kEnsBT * 11) +
+           sizeof(unsigned long long) * 2 * kEnsGroups * kEnsSlots + 16;  // barriers, counters, TMEM base, flag
+}
+static_assert(ens_smem_bytes(kEnsMaxU) <= 227 * 1024, "ensemble shared memory budget");
 
 struct EnsParams {
-    int n, np, kp;                // oscillators; rows padded to kEnsRT; K padded to kEnsKC
+    int n, np, kp;                // oscillators; allocated (padded) rows; K padded to kEnsKAlign
+    int n_rt;                     // row tiles of this launch
     int batch, bp;                // members, padded to kEnsBT
     int member0;                  // first member of this launch (host chunking)
     int n_in;
-    const double *w;              // np x kp row-major, zero padded
+    const double *w;              // fragment order, ens_w_index(); n_rt * TR * kp
     const double *w_in;           // n x n_in
     const double *consts;         // (batch, 11)
     double *m;                    // (batch, n, 3) in/out
@@ -54,19 +110,71 @@ struct EnsParams {
     double dt, h2, dt6;
     long long steps, stride, n_records;
     double *states;               // (n_records, batch, n, 3) or null
-    double *x;                    // [2][kp][bp] stage x
-    double *st;                   // [13][np][bp] RK state (SoA)
-    unsigned long long *bar;      // per member-column counters, 32 words apart
+    double *x;                    // [2][bp / 32][kp * 32] stage x, ens_x_index()
+    double *st;                   // [np][bp] cin (n_in > 1); the RK state lives in TMEM
+    unsigned long long *bar;      // per half-column counters, 32 words apart
     StatusDev *status;
+    int debug_solo;               // timeline experiments: group 1 idles (results of its members invalid)
 };
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+// Fragment-order layouts.  K is cut into 32-column chunks (the last one may be
+// shorter: kc = kp - 32*ch, a multiple of 8); nk = kc / 4 k-steps.
+// W: [row tile][chunk][row unit ru < U][k-step ks < nk][lane], lane = 4g + t
+//    holds W[row0 + 8ru + g][32ch + 4ks + t]   (A fragment of m8n8k4.row)
+// X: [half-column][chunk][k-step][member unit mu < 4][lane], lane = 4g + t
+//    holds X[32ch + 4ks + t][32 half + 8mu + g]   (B fragment of m8n8k4.col)
+__host__ __device__ inline size_t ens_x_index(int k, int bg, int kp) {
+    const int col = bg >> 5, bl = bg & 31;
+    return (size_t)col * kp * kEnsGW + (size_t)(k >> 5) * (kEnsKC * kEnsGW) +
+           (size_t)((((k & 31) >> 2) * 4 + (bl >> 3)) * 32 + (bl & 7) * 4 + (k & 3));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// ---- mbarrier / bulk-copy / DMMA primitives --------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "ENS_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra ENS_WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ bool mbar_test(unsigned long long *b, uint32_t parity) {  // non-blocking
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         unsigned long long *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void group_sync(int grp) {  // named barrier 1 + grp over one warp group
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kEnsGroupThreads) : "memory");
+}
+
 
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -74,199 +182,353 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void column_sync(unsigned long long *bar, unsigned long long target) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
-        unsigned long long v;
-        do {
-            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-        } while (v < target);
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    }
-    __syncthreads();
-}
-
 #ifdef STO_TIMELINE
-__device__ unsigned long long g_ens_timeline[16][4];
-#define ENS_TL(e, ev)                                                                 \
-    do {                                                                              \
-        if (blockIdx.x == 0 && threadIdx.x == 0 && (e) >= 40 && (e) < 56)             \
-            g_ens_timeline[(e) - 40][ev] = clock64();                                 \
+__device__ unsigned long long g_ens_timeline[16][8];  // [stage][event + 4 * group]
+#define ENS_TL(e, ev)                                                                         \
+    do {                                                                                      \
+        if (blockIdx.x == 0 && threadIdx.x % kEnsGroupThreads == 0 && (e) >= 40 && (e) < 56)   \
+            g_ens_timeline[(e) - 40][(ev) + 4 * grp] = clock64();                             \
     } while (0)
 #else
 #define ENS_TL(e, ev)
 #endif
 
+// ---- tensor-memory scratch (tcgen05.ld / tcgen05.st, 32x32b: one lane per thread) ----
+template <int N>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[N]);
+template <>
+__device__ __forceinline__ void tmem_ld<6>(uint32_t taddr, uint32_t (&r)[6]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr) : "memory");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+                 : "=r"(r[4]), "=r"(r[5]) : "r"(taddr + 4) : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_ld<18>(uint32_t taddr, uint32_t (&r)[18]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+                 : "=r"(r[16]), "=r"(r[17]) : "r"(taddr + 16) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st6(uint32_t taddr, V3 a, V3 b) {  // 2 doubles x 3 = 12 columns
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+        "r"(__double2loint(a.x)), "r"(__double2hiint(a.x)), "r"(__double2loint(a.y)), "r"(__double2hiint(a.y)),
+        "r"(__double2loint(a.z)), "r"(__double2hiint(a.z)), "r"(__double2loint(b.x)), "r"(__double2hiint(b.x))
+        : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr + 8),
+                 "r"(__double2loint(b.y)), "r"(__double2hiint(b.y)), "r"(__double2loint(b.z)),
+                 "r"(__double2hiint(b.z))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st3(uint32_t taddr, V3 a) {  // 6 columns
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
+                 "r"(__double2loint(a.x)), "r"(__double2hiint(a.x)), "r"(__double2loint(a.y)),
+                 "r"(__double2hiint(a.y))
+                 : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr + 4),
+                 "r"(__double2loint(a.z)), "r"(__double2hiint(a.z))
+                 : "memory");
+}
+__device__ __forceinline__ double u2d(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
+
+template <int U>
 __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_constant__ EnsParams p) {
+    constexpr int TR = 8 * U;
+    constexpr int WS = TR * kEnsKC;  // W part of a slot (doubles)
+    constexpr int SS = ens_slot_doubles(U);
+    constexpr int GW = kEnsGroupThreads / 32;  // warps per group
+    static_assert(U * kEnsTmemOut <= kEnsTmemCols / 4, "RK state of U outputs must fit a TMEM slice");
     extern __shared__ __align__(16) double smem[];
-    double *cs = smem + kEnsStages * kEnsBuf;  // [64][11] member consts
+    double *cpb = smem + kEnsGroups * kEnsSlots * SS;  // TR x kEnsLDB coupling sums
+    double *cs = cpb + TR * kEnsLDB;                   // [64][11] member consts
+    unsigned long long *full_all = reinterpret_cast<unsigned long long *>(cs + kEnsBT * 11);
+    unsigned *done_all = reinterpret_cast<unsigned *>(full_all + kEnsGroups * kEnsSlots);
+    uint32_t *tmem_base_slot = done_all + kEnsGroups * kEnsSlots;
+    volatile int *go = reinterpret_cast<volatile int *>(tmem_base_slot + 1);  // group 1 start gate
 
-    const int n_rt = p.np / kEnsRT;
-    const int rt = blockIdx.x % n_rt, ct = blockIdx.x / n_rt;  // row tile, member column
-    const int row0 = rt * kEnsRT, col0 = ct * kEnsBT;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wr = warp >> 2, wc = warp & 3;  // 4 row groups (16) x 4 member quarters (16)
-    const int g = lane >> 2, t = lane & 3;
-    unsigned long long *bar = p.bar + 32 * ct;
-    const size_t plane = (size_t)p.np * p.bp;   // one SoA state component
+    const int rt = blockIdx.x % p.n_rt, ct = blockIdx.x / p.n_rt;  // row tile, member column
+    const int row0 = rt * TR, col0 = ct * kEnsBT;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int grp = warp / GW, wl = warp % GW;  // warp group (member half), warp in group
+    const int hcol = 2 * ct + grp;              // global half-column
+    unsigned long long *bar = p.bar + 32 * hcol;
+    double *ring = smem + grp * kEnsSlots * SS;
+    unsigned long long *full = full_all + grp * kEnsSlots;
+    unsigned *done = done_all + grp * kEnsSlots;  // warps finished with the slot's current fill
     const size_t xplane = (size_t)p.kp * p.bp;  // one x buffer
+    const int n_chunks = (p.kp + kEnsKC - 1) / kEnsKC;
+    const int nring = min(kEnsSlots, n_chunks);  // slots in use: a refill is at most one stage ahead
+    const long long n_stages = 4 * p.steps;
+    const uint64_t pol = l2_policy_evict_last();  // W and X tiles are re-read by other CTAs
 
-    for (int i = threadIdx.x; i < kEnsBT * 11; i += blockDim.x) {
+    if (warp == 0) {  // whole TMEM for this CTA (1 CTA per SM)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_base_slot)),
+                     "n"(kEnsTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kEnsGroups * kEnsSlots; ++s) {
+            mbar_init(&full_all[s], 1);
+            done_all[s] = 0u;
+        }
+        *go = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < kEnsBT * 11; i += blockDim.x) {
         const int bl = i / 11, q = i % 11;
         const int b = min(p.member0 + col0 + bl, p.batch - 1);
         cs[i] = p.consts[(size_t)b * 11 + q];
     }
-    // ---- prologue: state and x(0) from m, record 0 -------------------------
-    for (int i = threadIdx.x; i < kEnsRT * kEnsBT; i += blockDim.x) {
-        const int rl = i / kEnsBT, bl = i % kEnsBT;
-        const int k = row0 + rl, bg = col0 + bl, b = p.member0 + bg;
-        double mx = 0.0, my = 0.0, mz = 0.0;
-        if (k < p.n && b < p.batch) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this thread's TMEM slice: lane 32*(warp%4) + lane, columns 128*(warp/4) ...
+    const uint32_t tmem = *tmem_base_slot + ((uint32_t)(32 * (warp & 3)) << 16) +
+                          (uint32_t)(kEnsTmemCols / 4) * (warp >> 2);
+
+    // chunk ch of the K loop in ring slot s: arm the barrier, copy W (and X)
+    auto kc_of = [&](int ch) { return min(kEnsKC, p.kp - ch * kEnsKC); };
+    const double *wtile = p.w + (size_t)rt * TR * p.kp;  // this row tile, fragment order
+    auto issue_w = [&](int s, int ch) {  // one thread; also arms full[s] for the W + X bytes
+        const int kc = kc_of(ch);
+        mbar_expect_tx(&full[s], (uint32_t)(TR + kEnsGW) * kc * 8);
+        bulk_g2s(ring + s * SS, wtile + (size_t)ch * TR * kEnsKC, (uint32_t)(TR * kc * 8), &full[s], pol);
+    };
+    auto issue_x = [&](int s, int ch, long long g) {  // one thread: X chunk of stage g (buffer g & 1)
+        const double *xsrc = p.x + (size_t)(g & 1) * xplane + (size_t)hcol * p.kp * kEnsGW;
+        bulk_g2s(ring + s * SS + WS, xsrc + (size_t)ch * kEnsKC * kEnsGW, (uint32_t)(kc_of(ch) * kEnsGW * 8),
+                 &full[s], pol);
+    };
+    // first warp of the group: wait until every row tile has published this half-column's
+    // x of stage g (counter >= (g+1) * n_rt), then issue the X parts of the ring's first chunks.
+    auto open_stage = [&](long long g) {
+        if (lane == 0) {
+            const unsigned long long target = (unsigned long long)(g + 1) * p.n_rt;
+            unsigned long long v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+            } while (v < target);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
+        const int s0 = (int)((g * n_chunks) % nring);
+        if (lane < nring) issue_x((s0 + lane) % nring, lane, g);
+    };
+
+    // ---- roles -------------------------------------------------------------------
+    const int mu = wl & 3, kph = wl >> 2;  // GEMM: member unit, k-step parity; epilogue: row half
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int bl = kEnsGW * grp + 8 * mu + g8, rsub = 4 * kph + t4;  // epilogue: member, row offset
+    const int bg = col0 + bl, b = p.member0 + bg;
+    const bool member_ok = b < p.batch;
+    const int bc = min(b, p.batch - 1);  // clamped for reads
+    const Consts c{cs[bl * 11 + 0], cs[bl * 11 + 1], cs[bl * 11 + 2], cs[bl * 11 + 3],
+                   cs[bl * 11 + 4], cs[bl * 11 + 5], cs[bl * 11 + 6], cs[bl * 11 + 7],
+                   cs[bl * 11 + 8], cs[bl * 11 + 9], cs[bl * 11 + 10]};
+    const double *samp = p.samples + (size_t)bc * p.sample_member_stride;
+
+    // ---- prologue: m -> TMEM, x(0), record 0 -----------------------------------
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+        const int k = row0 + rsub + 8 * j;
+        const bool ok = k < p.n && member_ok;
+        V3 m{0.0, 0.0, 0.0};
+        if (ok) {
             const double *mm = p.m + ((size_t)b * p.n + k) * 3;
-            mx = mm[0];
-            my = mm[1];
-            mz = mm[2];
+            m = V3{mm[0], mm[1], mm[2]};
             if (p.states) {
                 double *so = p.states + ((size_t)b * p.n + k) * 3;
-                so[0] = mx;
-                so[1] = my;
-                so[2] = mz;
+                so[0] = m.x;
+                so[1] = m.y;
+                so[2] = m.z;
             }
         }
-        const size_t o = (size_t)k * p.bp + bg;
-        p.st[0 * plane + o] = mx;
-        p.st[1 * plane + o] = my;
-        p.st[2 * plane + o] = mz;
-        if (k < p.kp) p.x[o] = mx;  // parity 0 (rows >= n stay zero)
+        tmem_st3(tmem + j * kEnsTmemOut, m);
+        if (ok) p.x[ens_x_index(k, bg, p.kp)] = m.x;  // parity 0 (padding stays zero)
     }
-    const int n_chunks = p.kp / kEnsKC;
-    long long epoch = 0;
-    column_sync(bar, (unsigned long long)(++epoch) * n_rt);
+    tmem_wait_st();
+    group_sync(grp);
+    if (wl == 0) {
+        if (lane == 0) {
+            __threadfence();
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+            // group 1 starts half a GEMM later (see header): wait for group 0's gate
+            if (grp == 1)
+                while (*go == 0) __nanosleep(64);
+        }
+        __syncwarp();
+        if (lane < nring) issue_w(lane, lane);
+        open_stage(0);
+    }
 
+    int slot = 0;
+    uint32_t phase = 0;
+    int ch_fill = nring;   // next chunk (within its stage) a refill loads
+    long long g_fill = 0;  // ... and its stage
+    if (ch_fill == n_chunks) {
+        ch_fill = 0;
+        g_fill = 1;
+    }
+    const int gate_chunk = n_chunks / 2;
     long long next_rec = p.stride, rec_idx = 1;
-    for (long long step = 1; step <= p.steps; ++step) {
+    long long gstage = 0;
+    for (long long step = 1; step <= (p.debug_solo && grp == 1 ? 0 : p.steps); ++step) {
         const bool record = (step == next_rec) || (step == p.steps);
         const long long sidx = p.n_samples == 1 ? 0 : (step - 1) / p.sps;
-        for (int stage = 0; stage < 4; ++stage) {
-            const double *xsrc = p.x + (size_t)((epoch - 1) & 1) * xplane;  // published last stage
-            ENS_TL(epoch, 0);
-            double acc[2][2][2];
+        for (int stage = 0; stage < 4; ++stage, ++gstage) {
+            ENS_TL(gstage, 0);
+            double acc[U][2];
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int r = 0; r < U; ++r) acc[r][0] = acc[r][1] = 0.0;
+#ifdef STO_TIMELINE
+            long long waited = 0;
+#endif
+            for (int ch = 0; ch < n_chunks; ++ch) {
+#ifdef STO_TIMELINE
+                const long long w0 = clock64();
+                mbar_wait(&full[slot], phase);
+                waited += clock64() - w0;
+#else
+                mbar_wait(&full[slot], phase);
+#endif
+                const double *W = ring + slot * SS;
+                const double *X = W + WS;
+                const int nk = kc_of(ch) >> 2;  // k-steps in this chunk (even)
+                if (nk == kEnsKC / 4) {
+                    // full chunk: compile-time offsets, fragments of the next k-step loaded
+                    // while the DMMAs of this one issue (register double buffer)
+                    constexpr int NQ = kEnsKC / 8;  // k-steps of this warp's parity
+                    double a[2][U], bf[2];
 #pragma unroll
-                for (int jj = 0; jj < 2; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
-            // ---- 3-stage cp.async pipeline over K --------------------------
-            auto load_chunk = [&](int c) {
-                double *ws = smem + (c % kEnsStages) * kEnsBuf;
-                double *xs = ws + kEnsRT * kEnsLD;
-                const int k0 = c * kEnsKC;
-                for (int i = threadIdx.x; i < (kEnsRT + kEnsKC) * 32; i += blockDim.x) {
-                    const int r = i >> 5, c2 = (i & 31) * 2;
-                    if (r < kEnsRT)
-                        cp_async16(ws + r * kEnsLD + c2, p.w + (size_t)(row0 + r) * p.kp + k0 + c2);
-                    else
-                        cp_async16(xs + (r - kEnsRT) * kEnsLD + c2,
-                                   xsrc + (size_t)(k0 + r - kEnsRT) * p.bp + col0 + c2);
-                }
-            };
+                    for (int r = 0; r < U; ++r) a[0][r] = W[(r * (kEnsKC / 4) + kph) * 32 + lane];
+                    bf[0] = X[(kph * 4 + mu) * 32 + lane];
 #pragma unroll
-            for (int c = 0; c < kEnsStages - 1; ++c) {
-                if (c < n_chunks) load_chunk(c);
-                cp_async_commit();
-            }
-            for (int c = 0; c < n_chunks; ++c) {
-                asm volatile("cp.async.wait_group %0;" ::"n"(kEnsStages - 2) : "memory");
-                __syncthreads();  // chunk c landed for everyone; chunk c-1 fully consumed
-                if (c + kEnsStages - 1 < n_chunks) load_chunk(c + kEnsStages - 1);
-                cp_async_commit();
-                const double *W = smem + (c % kEnsStages) * kEnsBuf;
-                const double *X = W + kEnsRT * kEnsLD;
-#pragma unroll 4
-                for (int kk = 0; kk < kEnsKC / 4; ++kk) {
-                    const double a0 = W[(wr * 16 + g) * kEnsLD + kk * 4 + t];
-                    const double a1 = W[(wr * 16 + 8 + g) * kEnsLD + kk * 4 + t];
-                    const double *xr = X + (kk * 4 + t) * kEnsLD + wc * 16 + g;
-                    const double b[2] = {xr[0], xr[8]};
+                    for (int q = 0; q < NQ; ++q) {
+                        if (q + 1 < NQ) {
+                            const int kn = 2 * (q + 1) + kph;
 #pragma unroll
-                    for (int jj = 0; jj < 2; ++jj) {
-                        dmma(acc[0][jj][0], acc[0][jj][1], a0, b[jj]);
-                        dmma(acc[1][jj][0], acc[1][jj][1], a1, b[jj]);
+                            for (int r = 0; r < U; ++r) a[(q + 1) & 1][r] = W[(r * (kEnsKC / 4) + kn) * 32 + lane];
+                            bf[(q + 1) & 1] = X[(kn * 4 + mu) * 32 + lane];
+                        }
+#pragma unroll
+                        for (int r = 0; r < U; ++r) dmma(acc[r][0], acc[r][1], a[q & 1][r], bf[q & 1]);
+                    }
+                } else {
+                    for (int kk = kph; kk < nk; kk += 2) {
+                        double a[U];
+#pragma unroll
+                        for (int r = 0; r < U; ++r) a[r] = W[(r * nk + kk) * 32 + lane];
+                        const double bf = X[(kk * 4 + mu) * 32 + lane];
+#pragma unroll
+                        for (int r = 0; r < U; ++r) dmma(acc[r][0], acc[r][1], a[r], bf);
                     }
                 }
+                // Slot consumed by this warp; the LAST of the group's warps to get here
+                // refills it (the slot's shared-memory reads are complete: their values
+                // fed the DMMAs above, so a relaxed counter suffices).  A chunk of the
+                // next stage gets only its W here; its X follows in open_stage.
+                __syncwarp();
+                if (lane == 0) {
+                    if (atomicAdd(&done[slot], 1u) % GW == GW - 1 && g_fill < n_stages) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue_w(slot, ch_fill);
+                        if (g_fill == gstage) issue_x(slot, ch_fill, g_fill);
+                    }
+                    if (grp == 0 && gstage == 0 && ch == gate_chunk && wl == 0) *go = 1;
+                }
+                if (++ch_fill == n_chunks) {
+                    ch_fill = 0;
+                    ++g_fill;
+                }
+                if (++slot == nring) {
+                    slot = 0;
+                    phase ^= 1;
+                }
             }
-            cp_async_wait_0();
-            __syncthreads();
-            ENS_TL(epoch, 1);
-            // ---- RK4 epilogue ------------------------------------------------
-            // accumulators -> shared [row][member] (pipeline buffers are idle now)
-            double *cpb = smem;  // 64 x kEnsLD
+            // ---- split-K reduction into cpb[row][member] --------------------
+            double *cpg = cpb + kEnsGW * grp + 8 * mu + 2 * t4;
+            if (kph == 1) {
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int jj = 0; jj < 2; ++jj) {
-                    const int rl = wr * 16 + i * 8 + g, bl = wc * 16 + jj * 8 + 2 * t;
-                    cpb[rl * kEnsLD + bl] = acc[i][jj][0];
-                    cpb[rl * kEnsLD + bl + 1] = acc[i][jj][1];
+                for (int r = 0; r < U; ++r) {
+                    double *d = cpg + (8 * r + g8) * kEnsLDB;
+                    d[0] = acc[r][0];
+                    d[1] = acc[r][1];
                 }
-            __syncthreads();
-            double *xdst = p.x + (size_t)(epoch & 1) * xplane;
-            // thread -> (row, member) with members fastest: coalesced SoA state
-#pragma unroll 2
-            for (int idx = threadIdx.x; idx < kEnsRT * kEnsBT; idx += blockDim.x) {
-                const int rl = idx / kEnsBT, bl = idx % kEnsBT;
-                const int k = row0 + rl, bg = col0 + bl, b = p.member0 + bg;
-                if (k >= p.n || b >= p.batch) continue;
-                const size_t o = (size_t)k * p.bp + bg;
-                const double *cc = cs + bl * 11;
-                const Consts c{cc[0], cc[1], cc[2], cc[3], cc[4], cc[5],
-                               cc[6], cc[7], cc[8], cc[9], cc[10]};
-                // batch every state load of this output before the arithmetic
-                const V3 m{p.st[0 * plane + o], p.st[1 * plane + o], p.st[2 * plane + o]};
-                V3 cur = m, a{0.0, 0.0, 0.0}, q{0.0, 0.0, 0.0};
-                if (stage > 0) cur = V3{p.st[3 * plane + o], p.st[4 * plane + o], p.st[5 * plane + o]};
-                if (stage == 1 || stage == 3)
-                    a = V3{p.st[6 * plane + o], p.st[7 * plane + o], p.st[8 * plane + o]};
-                if (stage == 3) q = V3{p.st[9 * plane + o], p.st[10 * plane + o], p.st[11 * plane + o]};
-                double cin;
+            }
+            group_sync(grp);
+            if (kph == 0) {
+#pragma unroll
+                for (int r = 0; r < U; ++r) {
+                    double *d = cpg + (8 * r + g8) * kEnsLDB;
+                    d[0] = acc[r][0] + d[0];
+                    d[1] = acc[r][1] + d[1];
+                }
+            }
+            group_sync(grp);
+            ENS_TL(gstage, 1);
+#ifdef STO_TIMELINE
+            if (blockIdx.x == 0 && threadIdx.x % kEnsGroupThreads == 0 && gstage >= 40 && gstage < 56)
+                g_ens_timeline[gstage - 40][3 + 4 * grp] = waited;
+#endif
+            // ---- RK4 epilogue: U outputs per thread, state in TMEM ---------------
+            double *xdst = p.x + (size_t)((gstage + 1) & 1) * xplane;
+            const bool last_stage = (gstage + 1 == n_stages);
+            const double h = stage == 2 ? p.dt : p.h2;
+#pragma unroll kEnsEpiUnroll
+            for (int j = 0; j < U; ++j) {
+                const int rl = rsub + 8 * j;
+                const int k = row0 + rl;
+                const bool ok = k < p.n && member_ok;
+                const uint32_t ta = tmem + j * kEnsTmemOut;
+                V3 m, a{0.0, 0.0, 0.0}, cur;
                 if (stage == 0) {
-                    const double *u = p.samples + (size_t)b * p.sample_member_stride +
-                                      (size_t)sidx * p.n_in;
-                    cin = (p.n_in == 1) ? rmul(p.w_in[k], u[0])
-                                        : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
-                    p.st[12 * plane + o] = cin;
+                    uint32_t r[6];
+                    tmem_ld<6>(ta, r);
+                    tmem_wait_ld();
+                    m = V3{u2d(r[0], r[1]), u2d(r[2], r[3]), u2d(r[4], r[5])};
+                    cur = m;
                 } else {
-                    cin = p.st[12 * plane + o];
+                    uint32_t r[18];
+                    tmem_ld<18>(ta, r);
+                    tmem_wait_ld();
+                    m = V3{u2d(r[0], r[1]), u2d(r[2], r[3]), u2d(r[4], r[5])};
+                    a = V3{u2d(r[6], r[7]), u2d(r[8], r[9]), u2d(r[10], r[11])};
+                    cur = V3{u2d(r[12], r[13]), u2d(r[14], r[15]), u2d(r[16], r[17])};
                 }
-                const V3 d = row_rhs(cur, cpb[rl * kEnsLD + bl], cin, c);
+                double cin = 0.0;
+                if (k < p.n) {
+                    if (p.n_in == 1) {  // recomputed every stage (u is held): same rounding as storing it
+                        cin = rmul(p.w_in[k], samp[(size_t)sidx]);
+                    } else if (stage == 0) {
+                        cin = tree_dot_stream(p.w_in + (size_t)k * p.n_in, samp + (size_t)sidx * p.n_in, p.n_in);
+                        p.st[(size_t)k * p.bp + bg] = cin;
+                    } else {
+                        cin = p.st[(size_t)k * p.bp + bg];
+                    }
+                }
+                const V3 d = row_rhs(cur, cpb[rl * kEnsLDB + bl], cin, c);
                 double xpub;
                 if (stage < 3) {
-                    if (stage == 0) {
-                        p.st[6 * plane + o] = d.x;
-                        p.st[7 * plane + o] = d.y;
-                        p.st[8 * plane + o] = d.z;
-                    } else if (stage == 1) {
-                        const V3 a2 = acc_k2(a, d);
-                        p.st[6 * plane + o] = a2.x;
-                        p.st[7 * plane + o] = a2.y;
-                        p.st[8 * plane + o] = a2.z;
-                    } else {
-                        p.st[9 * plane + o] = d.x;
-                        p.st[10 * plane + o] = d.y;
-                        p.st[11 * plane + o] = d.z;
-                    }
-                    const V3 sp = stage_point(m, d, stage == 2 ? p.dt : p.h2);
-                    p.st[3 * plane + o] = sp.x;
-                    p.st[4 * plane + o] = sp.y;
-                    p.st[5 * plane + o] = sp.z;
+                    // acc: k1 | k1 + k2*2 | (k1 + k2*2) + k3*2
+                    const V3 a2 = stage == 0 ? d : acc_k2(a, d);
+                    const V3 sp = stage_point(m, d, h);
+                    tmem_st6(ta + 6, a2, sp);
                     xpub = sp.x;
                 } else {
-                    const V3 mn = rk4_final(m, a, q, d, p.dt6);
-                    p.st[0 * plane + o] = mn.x;
-                    p.st[1 * plane + o] = mn.y;
-                    p.st[2 * plane + o] = mn.z;
+                    const V3 mn{radd(m.x, rmul(radd(a.x, d.x), p.dt6)), radd(m.y, rmul(radd(a.y, d.y), p.dt6)),
+                                radd(m.z, rmul(radd(a.z, d.z), p.dt6))};
+                    tmem_st3(ta, mn);
                     xpub = mn.x;
-                    if (record) {
+                    if (record && ok) {
                         if (!all_finite(mn)) {
                             // key: step, member, oscillator (lexicographic min)
                             atomicMin(&p.status->key, (step << 40) | ((long long)b << 20) | k);
@@ -279,32 +541,40 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
                             so[2] = mn.z;
                         }
                     }
+                    if (last_stage && ok) {
+                        double *mm = p.m + ((size_t)b * p.n + k) * 3;
+                        mm[0] = mn.x;
+                        mm[1] = mn.y;
+                        mm[2] = mn.z;
+                    }
                 }
-                xdst[o] = xpub;
+                if (ok) xdst[ens_x_index(k, bg, p.kp)] = xpub;
             }
-            ENS_TL(epoch, 2);
-            ++epoch;
-            if (!(step == p.steps && stage == 3)) column_sync(bar, (unsigned long long)epoch * n_rt);
-            ENS_TL(epoch - 1, 3);
+            tmem_wait_st();
+            ENS_TL(gstage, 2);
+            if (!last_stage) {
+                group_sync(grp);  // this group's x rows are written; its cpb half is free again
+                if (wl == 0) {
+                    if (lane == 0) {
+                        __threadfence();
+                        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+                    }
+                    open_stage(gstage + 1);
+                }
+            }
         }
         if (record && step == next_rec) {
             next_rec += p.stride;
             ++rec_idx;
         }
     }
-    // ---- epilogue: final m ------------------------------------------------
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    for (int i = threadIdx.x; i < kEnsRT * kEnsBT; i += blockDim.x) {
-        const int rl = i / kEnsBT, bl = i % kEnsBT;
-        const int k = row0 + rl, bg = col0 + bl, b = p.member0 + bg;
-        if (k < p.n && b < p.batch) {
-            const size_t o = (size_t)k * p.bp + bg;
-            double *mm = p.m + ((size_t)b * p.n + k) * 3;
-            mm[0] = p.st[0 * plane + o];
-            mm[1] = p.st[1 * plane + o];
-            mm[2] = p.st[2 * plane + o];
-        }
-    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_slot),
+                     "n"(kEnsTmemCols)
+                     : "memory");
 }
 
 }  // namespace sto

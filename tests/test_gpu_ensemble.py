@@ -88,3 +88,76 @@ def test_ensemble_divergence_reports_member(sto):
                                                           record_stride=5))
     assert info.value.member == 3
     assert info.value.step == 5 and info.value.oscillator == 0
+
+
+def _rand_top(sto, n, n_in=1, seed=0):
+    g = np.random.default_rng(seed)
+    w = g.uniform(-1, 1, (n, n)) / np.sqrt(max(n, 3) / 3.0)
+    np.fill_diagonal(w, 0.0)
+    return sto.Topology(sto.CouplingMatrix(w), sto.InputWeights(g.uniform(-1, 1, (n, n_in))))
+
+
+def _check_members(sto, oracle_mod, top, params, cfg, members, series=None):
+    ens = sto.integrate_ensemble(top, params, cfg)
+    n = cfg.n
+    samples = cfg.input_series.samples if cfg.input_series is not None else np.zeros((1, top.n_in))
+    sps = cfg.input_series.steps_per_sample if cfg.input_series is not None else 1
+    worst = 0.0
+    for b in members:
+        want, _ = oracle_mod.integrate(top.coupling.entries, top.input_weights.entries,
+                                       sto.kernel_scalars(params[b]), sto.initial_state(n),
+                                       samples, sps, cfg.dt, cfg.steps, cfg.record_stride)
+        dev = float(np.abs(ens.states[:, b] - want).max())
+        worst = max(worst, dev)
+        assert dev <= TOL, f"member {b}: deviation {dev:.3e}"
+    return worst
+
+
+@pytest.mark.parametrize("u", range(1, 8))
+def test_every_tile_height(sto, oracle_mod, monkeypatch, u):
+    """Force each CTA tile height TR = 8U (STO_ENS_U); n = 203 leaves a ragged last tile
+    and a K tail that is not a multiple of the 32-column chunk."""
+    monkeypatch.setenv("STO_ENS_U", str(u))
+    n, batch, steps = 203, 70, 150
+    top = _rand_top(sto, n, seed=u)
+    params = _sweep(sto, batch)
+    cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=50)
+    _check_members(sto, oracle_mod, top, params, cfg, [0, 33, 63, 64, 69])
+
+
+@pytest.mark.parametrize("n,batch", [(1, 3), (7, 130), (8, 64), (33, 65), (1001, 4)])
+def test_ragged_sizes(sto, oracle_mod, n, batch):
+    top = _rand_top(sto, n, seed=n)
+    params = _sweep(sto, batch)
+    series = sto.InputSeries(np.random.default_rng(n).uniform(-1, 1, (20, 1)), 10)
+    cfg = sto.RunConfig(n=n, steps=200, dt=1e-11, record_stride=40, input_series=series)
+    members = sorted({0, batch // 2, batch - 1})
+    _check_members(sto, oracle_mod, top, params, cfg, members)
+
+
+def test_multichannel_input(sto, oracle_mod):
+    n, n_in = 150, 3
+    top = _rand_top(sto, n, n_in=n_in, seed=9)
+    params = _sweep(sto, 20)
+    series = sto.InputSeries(np.random.default_rng(9).uniform(-1, 1, (25, n_in)), 4)
+    cfg = sto.RunConfig(n=n, steps=100, dt=1e-11, record_stride=25, input_series=series)
+    _check_members(sto, oracle_mod, top, params, cfg, [0, 7, 19])
+
+
+def test_several_launches(sto, oracle_mod):
+    """n = 2000, B = 1024: more member columns than fit one wave of CTAs -> the host
+    splits the batch into several persistent launches (member0 offsets)."""
+    n, batch = 2000, 1024
+    top = _rand_top(sto, n, seed=4)
+    params = _sweep(sto, batch)
+    cfg = sto.RunConfig(n=n, steps=20, dt=1e-11, record_stride=10)
+    _check_members(sto, oracle_mod, top, params, cfg, [0, 300, 511, 512, 1023])
+
+
+def test_repeat_runs_identical(sto):
+    top = _rand_top(sto, 300, seed=6)
+    params = _sweep(sto, 100)
+    cfg = sto.RunConfig(n=300, steps=60, dt=1e-11, record_stride=20)
+    a = sto.integrate_ensemble(top, params, cfg).states
+    b = sto.integrate_ensemble(top, params, cfg).states
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))

@@ -14,9 +14,14 @@ if top is None:
 params = [sto.PhysicalParams(current=c) for c in np.linspace(2e-3, 3e-3, B)]
 cfg = sto.RunConfig(n=n, steps=30, dt=1e-11, record_stride=30)
 sto.integrate_ensemble(top, params, cfg)
-buf = (ctypes.c_ulonglong * 64)()
-nat.lib().sto_debug_ens_timeline(buf, 64)
-t = np.array(buf, dtype=np.float64).reshape(16, 4)
+buf = (ctypes.c_ulonglong * 128)()
+nat.lib().sto_debug_ens_timeline(buf, 128)
+t = np.array(buf, dtype=np.float64).reshape(16, 2, 4)
+t0 = t[0, 0, 0]
 for s in range(15):
-    d = np.diff(t[s])
-    print(f"epoch {40+s}: gemm {d[0]:7.0f}  epilogue {d[1]:7.0f}  sync {d[2]:7.0f}  stage total {t[s+1,0]-t[s,0]:7.0f} cyc")
+    line = f"stage {40+s}:"
+    for g in range(2):
+        gemm, epi, total = t[s, g, 1] - t[s, g, 0], t[s, g, 2] - t[s, g, 1], t[s + 1, g, 0] - t[s, g, 0]
+        line += (f" | g{g} start {t[s, g, 0] - t0:8.0f} gemm {gemm:6.0f} (data wait {t[s, g, 3]:6.0f}) epi {epi:6.0f}"
+                 f" exch {total - gemm - epi:6.0f} total {total:6.0f}")
+    print(line)
