@@ -89,7 +89,7 @@ constexpr int kEnsKAlign = 8;                   // K padded to 8: chunk bytes % 
 __host__ __device__ constexpr int ens_slot_doubles(int u) { return 8 * u * kEnsKC + kEnsKC * kEnsGW; }
 __host__ __device__ constexpr size_t ens_smem_bytes(int u) {
     return sizeof(double) * ((size_t)kEnsGroups * kEnsSlots * ens_slot_doubles(u) + 8 * u * kEnsLDB +
-                             kEnsBT * 11) +
+                             kEnsBT * 11 + 8 * u) +
            sizeof(unsigned long long) * 2 * kEnsGroups * kEnsSlots + 16;  // barriers, counters, TMEM base, flag
 }
 static_assert(ens_smem_bytes(kEnsMaxU) <= 227 * 1024, "ensemble shared memory budget");
@@ -248,7 +248,8 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
     extern __shared__ __align__(16) double smem[];
     double *cpb = smem + kEnsGroups * kEnsSlots * SS;  // TR x kEnsLDB coupling sums
     double *cs = cpb + TR * kEnsLDB;                   // [64][11] member consts
-    unsigned long long *full_all = reinterpret_cast<unsigned long long *>(cs + kEnsBT * 11);
+    double *wins = cs + kEnsBT * 11;                   // [TR] input weights of the tile's rows (n_in = 1)
+    unsigned long long *full_all = reinterpret_cast<unsigned long long *>(wins + TR);
     unsigned *done_all = reinterpret_cast<unsigned *>(full_all + kEnsGroups * kEnsSlots);
     uint32_t *tmem_base_slot = done_all + kEnsGroups * kEnsSlots;
     volatile int *go = reinterpret_cast<volatile int *>(tmem_base_slot + 1);  // group 1 start gate
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
         const int b = min(p.member0 + col0 + bl, p.batch - 1);
         cs[i] = p.consts[(size_t)b * 11 + q];
     }
+    for (int i = tid; i < TR; i += blockDim.x) wins[i] = (row0 + i < p.n) ? p.w_in[(size_t)(row0 + i) * p.n_in] : 0.0;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -314,9 +316,12 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
         if (lane == 0) {
             const unsigned long long target = (unsigned long long)(g + 1) * p.n_rt;
             unsigned long long v;
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-            } while (v < target);
+            while (true) {  // relaxed polling with back-off, one acquire fence at the end
+                asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+                if (v >= target) break;
+                __nanosleep(64);
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         __syncwarp();
@@ -386,6 +391,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
         const long long sidx = p.n_samples == 1 ? 0 : (step - 1) / p.sps;
         for (int stage = 0; stage < 4; ++stage, ++gstage) {
             ENS_TL(gstage, 0);
+            const double u1 = (p.n_in == 1) ? samp[(size_t)sidx] : 0.0;  // lands during the GEMM
             double acc[U][2];
 #pragma unroll
             for (int r = 0; r < U; ++r) acc[r][0] = acc[r][1] = 0.0;
@@ -507,7 +513,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
                 double cin = 0.0;
                 if (k < p.n) {
                     if (p.n_in == 1) {  // recomputed every stage (u is held): same rounding as storing it
-                        cin = rmul(p.w_in[k], samp[(size_t)sidx]);
+                        cin = rmul(wins[rl], u1);
                     } else if (stage == 0) {
                         cin = tree_dot_stream(p.w_in + (size_t)k * p.n_in, samp + (size_t)sidx * p.n_in, p.n_in);
                         p.st[(size_t)k * p.bp + bg] = cin;
