@@ -350,7 +350,7 @@ def run_ours_ensemble(args, rank, world, local_rank):
                        "record_stride": stride, "dt": DT,
                        "parallelism": f"batch-sharded x{world}" if world > 1 else "1 GPU",
                        "kernel": "ens_rk4_kernel (DMMA m8n8k4 f64)",
-                       "l2": "W 8 MB + state 49 MB L2-resident by design; one launch per run"},
+                       "l2": "W 8 MB + stage x 8 MB L2-resident (fragment order), RK state in TMEM; one launch per run"},
             "e2e": {"value": batch_total * n * steps / e2e_s, "unit": "osc-steps/s",
                     "h2d_bytes_per_step": 8 * (n * n + n + batch * 3 * n + batch * 11),
                     "d2h_bytes_per_step": 8 * ens.states.size},
