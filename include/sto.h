@@ -190,6 +190,23 @@ STO_API int sto_integrate_host(sto_plan *plan, double *m, const double *samples,
 STO_API int sto_tree_matvec(int device, int64_t rows, int64_t cols, const double *a, int64_t lda,
                     const double *x, double *out);
 
+/* Reservoir construction on the device (topology.py:27-54 RngStream,
+ * :241-273 generate_coupling / generate_input_weights, :146-238 spectral_radius
+ * matvecs).  pcg = {state_hi, state_lo, inc_hi, inc_lo} of numpy's PCG64(seed)
+ * (bit_generator.state).  sto_pcg64_fill writes draws offset .. offset+count-1
+ * of Generator(PCG64).random() mapped to 2u - 1 -- bit-identical to
+ * RngStream.uniform_pm1 -- into out[0..count) or, when diag_n > 0, draws
+ * 0 .. n(n-1)-1 row-major onto the off-diagonal of the (n, ld) matrix out
+ * (diagonal set to 0).  All pointers device; asynchronous on `stream`. */
+STO_API int sto_pcg64_fill(int device, double *out, int64_t count, int64_t offset,
+                           const uint64_t pcg[4], int64_t diag_n, int64_t ld, void *stream);
+/* y = W x (row-major (rows, ld), device), unpinned summation order: the
+ * Arnoldi matvecs of the spectral-radius estimate.  Asynchronous. */
+STO_API int sto_gemv(int device, const double *w, int64_t rows, int64_t cols, int64_t ld,
+                     const double *x, double *y, void *stream);
+/* a[i] /= divisor (IEEE), device, asynchronous: `entries /= rho`. */
+STO_API int sto_scale_div(int device, double *a, int64_t count, double divisor, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

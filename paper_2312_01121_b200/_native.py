@@ -96,6 +96,13 @@ SIGNATURES = {
                                           ctypes.POINTER(Status)]),
     "sto_tree_matvec": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
                                        _c_double_p, ctypes.c_int64, _c_double_p, _c_double_p]),
+    "sto_pcg64_fill": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.POINTER(ctypes.c_uint64),
+                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]),
+    "sto_gemv": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "sto_scale_div": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                     ctypes.c_double, ctypes.c_void_p]),
 }
 
 _lib = None
@@ -158,25 +165,62 @@ def _stream_ptr(device: int):
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+def pcg64_words(seed: int) -> tuple[int, int, int, int]:
+    """(state_hi, state_lo, inc_hi, inc_lo) of numpy's PCG64(seed) before any draw."""
+    st = np.random.PCG64(seed).state["state"]
+    m64 = (1 << 64) - 1
+    return (st["state"] >> 64, st["state"] & m64, st["inc"] >> 64, st["inc"] & m64)
+
+
+def pcg64_fill(out, count: int, offset: int, words, diag_n: int = 0, ld: int = 0) -> None:
+    """Device draws of RngStream.uniform_pm1 (sto_pcg64_fill); `out` a CUDA float64 tensor."""
+    w = (ctypes.c_uint64 * 4)(*[int(v) for v in words])
+    dev = out.device.index
+    check(lib().sto_pcg64_fill(dev, out.data_ptr(), int(count), int(offset), w, int(diag_n),
+                               int(ld), _stream_ptr(dev)))
+
+
+def gemv(w, x, y) -> None:
+    """y = w @ x on the device (unpinned order; spectral-radius matvecs)."""
+    dev = w.device.index
+    check(lib().sto_gemv(dev, w.data_ptr(), w.shape[0], w.shape[1], w.stride(0), x.data_ptr(),
+                         y.data_ptr(), _stream_ptr(dev)))
+
+
+def scale_div(a, divisor: float) -> None:
+    """a /= divisor in place (IEEE division) on the device."""
+    dev = a.device.index
+    check(lib().sto_scale_div(dev, a.data_ptr(), a.numel(), float(divisor), _stream_ptr(dev)))
+
+
 class Plan:
     """Owns a device-resident W layout + launch configuration (sto_plan)."""
 
-    def __init__(self, w_cp: np.ndarray, w_in: np.ndarray, consts, device: int = 0,
+    def __init__(self, w_cp, w_in: np.ndarray, consts, device: int = 0,
                  flags: int = 0, shard: tuple[int, int, int, int] | None = None):
         """shard = (row_begin, row_count, world, rank): w_cp / w_in hold only the
-        shard's rows (row_count x n and row_count x n_in)."""
-        w_cp = np.ascontiguousarray(w_cp, dtype=np.float64)
+        shard's rows (row_count x n and row_count x n_in).  w_cp may be a host
+        array or a CUDA float64 tensor (device-built W: no host round trip)."""
+        if hasattr(w_cp, "data_ptr") and getattr(w_cp, "is_cuda", False):
+            w_cp = w_cp.contiguous()  # device-resident W (keeps the tensor alive below)
+            if w_cp.dtype != _torch().float64 or w_cp.device.index != int(device):
+                raise ParameterError("device coupling must be float64 on the plan's device")
+            w_ptr, shape = w_cp.data_ptr(), tuple(w_cp.shape)
+        else:
+            w_cp = np.ascontiguousarray(w_cp, dtype=np.float64)
+            w_ptr, shape = w_cp.ctypes.data, w_cp.shape
         w_in = np.ascontiguousarray(w_in, dtype=np.float64)
-        n = w_cp.shape[1]
-        rows = w_cp.shape[0]
-        if w_cp.ndim != 2 or (shard is None and rows != n):
+        if len(shape) != 2:
+            raise ParameterError("coupling matrix must be square")
+        rows, n = shape
+        if shard is None and rows != n:
             raise ParameterError("coupling matrix must be square")
         if w_in.ndim != 2 or w_in.shape[0] != rows:
             raise ParameterError("input weights must be (n, n_in)")
         self.n, self.n_in = n, w_in.shape[1]
         self.device = int(device)
         self.shard = shard
-        d = PlanDesc(n=self.n, n_in=self.n_in, w_cp=w_cp.ctypes.data, ld_cp=self.n,
+        d = PlanDesc(n=self.n, n_in=self.n_in, w_cp=w_ptr, ld_cp=self.n,
                      w_in=w_in.ctypes.data, ld_in=self.n_in, device=self.device, flags=flags)
         if shard is not None:
             d.row_begin, d.row_count, d.world, d.rank = (int(v) for v in shard)

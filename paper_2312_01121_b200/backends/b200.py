@@ -70,7 +70,9 @@ class B200Backend:
         self._torch = torch
         self._dev = torch.device("cuda", self.device_index)
         self.n, self.n_in = topology.n, topology.n_in
-        self._plan = _native.Plan(topology.coupling.entries, topology.input_weights.entries,
+        w = getattr(topology.coupling, "tensor", None)  # device-built W: used in place
+        self._plan = _native.Plan(w if w is not None else topology.coupling.entries,
+                                  topology.input_weights.entries,
                                   kernel_scalars(params) if consts is None else consts,
                                   device=self.device_index, flags=flags)
         self.last_kernel_seconds = float("nan")

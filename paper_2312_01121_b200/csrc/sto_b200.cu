@@ -13,6 +13,7 @@
 #include "sto_kernels.cuh"
 #include "sto_reg_kernel.cuh"
 #include "sto_ensemble_kernel.cuh"
+#include "sto_build.cuh"
 
 using namespace sto;
 
@@ -966,5 +967,52 @@ STO_API int sto_debug_timeline(unsigned long long *out, int count) {
     return STO_OK;
 }
 #endif
+
+// ---- reservoir construction on the device (sto_build.cuh) ------------------
+int sto_pcg64_fill(int device, double *out, int64_t count, int64_t offset, const uint64_t pcg[4],
+                   int64_t diag_n, int64_t ld, void *stream) {
+    if (!out || !pcg || count < 0 || offset < 0 || (diag_n > 0 && (count != diag_n * (diag_n - 1) || ld < diag_n)))
+        return fail(STO_E_PARAM, "sto_pcg64_fill: bad arguments");
+    STO_CUDA(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)stream;
+    Pcg64 g;
+    g.state = ((u128)pcg[0] << 64) | (u128)pcg[1];
+    g.inc = ((u128)pcg[2] << 64) | (u128)pcg[3];
+    u128 a32, c32;
+    pcg_jump_coeffs(g.inc, 32, a32, c32);
+    if (diag_n > 0) {
+        zero_diag_kernel<<<256, 256, 0, s>>>(out, diag_n, ld);
+        STO_CUDA(cudaGetLastError());
+    }
+    if (count > 0) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const long long warps_needed = (count + 4095) / 4096;  // >= 128 draws per lane
+        const int blocks = (int)std::max<long long>(1, std::min<long long>(8LL * sms, (warps_needed + 7) / 8));
+        pcg64_fill_kernel<<<blocks, 256, 0, s>>>(out, count, offset, g, diag_n, ld, a32, c32);
+        STO_CUDA(cudaGetLastError());
+    }
+    return STO_OK;
+}
+
+int sto_gemv(int device, const double *w, int64_t rows, int64_t cols, int64_t ld, const double *x,
+             double *y, void *stream) {
+    if (!w || !x || !y || rows < 0 || cols < 0 || ld < cols) return fail(STO_E_PARAM, "sto_gemv: bad arguments");
+    STO_CUDA(cudaSetDevice(device));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int blocks = (int)std::max<long long>(1, std::min<long long>(4LL * sms, (rows + 7) / 8));
+    gemv_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(w, rows, cols, ld, x, y);
+    STO_CUDA(cudaGetLastError());
+    return STO_OK;
+}
+
+int sto_scale_div(int device, double *a, int64_t count, double divisor, void *stream) {
+    if (!a || count < 0) return fail(STO_E_PARAM, "sto_scale_div: bad arguments");
+    STO_CUDA(cudaSetDevice(device));
+    scale_div_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(a, count, divisor);
+    STO_CUDA(cudaGetLastError());
+    return STO_OK;
+}
 
 }  // extern "C"

@@ -19,7 +19,7 @@ HEADER = ROOT / "include" / "sto.h"
 def declared_functions() -> list[str]:
     text = HEADER.read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(sto_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(sto_[a-z0-9_]+)\s*\(", text)))
 
 
 @pytest.fixture(scope="module")

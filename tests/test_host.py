@@ -254,3 +254,39 @@ def test_trajectory_csv_round_trip(tmp_path, params):
     t, k, mx, my, mz = lines[-1].split(",")
     assert float(t) == traj.times[-1] and int(k) == 1
     assert (float(mx), float(my), float(mz)) == tuple(traj.states[-1, 1])
+
+
+def _pcg_restated(state: int, inc: int, count: int, offset: int = 0) -> np.ndarray:
+    """Pure-Python PCG-XSL-RR 128/64 with LCG jump-ahead -- the formulas the device
+    kernel (csrc/sto_build.cuh) implements -- mapped to 2u - 1."""
+    mask = (1 << 128) - 1
+    mult = 0x2360ED051FC65DA44385DF649FCCF645
+    # jump `offset` steps
+    acc_m, acc_p, cur_m, cur_p, d = 1, 0, mult, inc, offset
+    while d:
+        if d & 1:
+            acc_m, acc_p = (acc_m * cur_m) & mask, (acc_p * cur_m + cur_p) & mask
+        cur_p, cur_m, d = ((cur_m + 1) * cur_p) & mask, (cur_m * cur_m) & mask, d >> 1
+    state = (acc_m * state + acc_p) & mask
+    out = np.empty(count)
+    for i in range(count):
+        state = (state * mult + inc) & mask
+        x = ((state >> 64) ^ state) & ((1 << 64) - 1)
+        rot = state >> 122
+        x = ((x >> rot) | (x << ((64 - rot) & 63))) & ((1 << 64) - 1)
+        out[i] = 2.0 * ((x >> 11) * 2.0 ** -53) - 1.0
+    return out
+
+
+@pytest.mark.parametrize("seed", [0, 5, 2**33 + 1])
+def test_pcg64_restatement_matches_numpy(seed):
+    """Pins the device PCG64 formulas (step-then-output, XSL-RR, jump-ahead) on the
+    CPU against numpy's Generator(PCG64(seed)) -- the reference's RngStream."""
+    from paper_2312_01121_b200 import RngStream, _native
+
+    hi, lo, ihi, ilo = _native.pcg64_words(seed)
+    state, inc = (hi << 64) | lo, (ihi << 64) | ilo
+    rs = RngStream(seed)
+    assert np.array_equal(_pcg_restated(state, inc, 20), rs.uniform_pm1(20))
+    rs.uniform_pm1(977)
+    assert np.array_equal(_pcg_restated(state, inc, 5, offset=997), rs.uniform_pm1(5))
