@@ -207,6 +207,14 @@ STO_API int sto_gemv(int device, const double *w, int64_t rows, int64_t cols, in
 /* a[i] /= divisor (IEEE), device, asynchronous: `entries /= rho`. */
 STO_API int sto_scale_div(int device, double *a, int64_t count, double divisor, void *stream);
 
+/* Recorded states as CSV text (integrator.py:217-225 write_trajectory_csv):
+ * header "t,k,mx,my,mz", then one row per (record i, oscillator k) in that
+ * order, every float as Python's f"{x:.17g}" (byte-identical), formatted by
+ * `threads` host threads (<= 0: all cores).  times (n_records,), states
+ * (n_records, n, 3): HOST pointers.  STO_E_PARAM on bad arguments / IO error. */
+STO_API int sto_write_trajectory_csv(const char *path, const double *times, const double *states,
+                                     int64_t n_records, int64_t n, int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

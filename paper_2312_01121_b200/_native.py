@@ -103,6 +103,8 @@ SIGNATURES = {
                                 ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "sto_scale_div": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.c_double, ctypes.c_void_p]),
+    "sto_write_trajectory_csv": (ctypes.c_int, [ctypes.c_char_p, _c_double_p, _c_double_p,
+                                                ctypes.c_int64, ctypes.c_int64, ctypes.c_int32]),
 }
 
 _lib = None
@@ -178,6 +180,19 @@ def pcg64_fill(out, count: int, offset: int, words, diag_n: int = 0, ld: int = 0
     dev = out.device.index
     check(lib().sto_pcg64_fill(dev, out.data_ptr(), int(count), int(offset), w, int(diag_n),
                                int(ld), _stream_ptr(dev)))
+
+
+def write_trajectory_csv(path, times: np.ndarray, states: np.ndarray, threads: int = 0) -> None:
+    """Native parallel `t,k,mx,my,mz` writer (sto_write_trajectory_csv)."""
+    t = np.ascontiguousarray(times, dtype=np.float64)
+    s = np.ascontiguousarray(states, dtype=np.float64)
+    if s.ndim != 3 or s.shape[2] != 3 or t.shape != (s.shape[0],):
+        raise ParameterError("write_trajectory_csv expects times (R,) and states (R, n, 3)")
+    rc = lib().sto_write_trajectory_csv(os.fsencode(path), t.ctypes.data_as(_c_double_p),
+                                        s.ctypes.data_as(_c_double_p), s.shape[0], s.shape[1],
+                                        int(threads))
+    if rc != STO_OK:
+        raise ParameterError(f"cannot write trajectory CSV to {path!s}")
 
 
 def gemv(w, x, y) -> None:

@@ -290,3 +290,40 @@ def test_pcg64_restatement_matches_numpy(seed):
     assert np.array_equal(_pcg_restated(state, inc, 20), rs.uniform_pm1(20))
     rs.uniform_pm1(977)
     assert np.array_equal(_pcg_restated(state, inc, 5, offset=997), rs.uniform_pm1(5))
+
+
+def _reference_csv_text(times, states) -> str:
+    """The reference's write_trajectory_csv loop (integrator.py:217-225), restated."""
+    lines = ["t,k,mx,my,mz\n"]
+    for i in range(states.shape[0]):
+        t = times[i]
+        for k in range(states.shape[1]):
+            mx, my, mz = states[i, k]
+            lines.append(f"{t:.17g},{k},{mx:.17g},{my:.17g},{mz:.17g}\n")
+    return "".join(lines)
+
+
+@pytest.mark.parametrize("threads", [1, 3, 0])
+def test_native_csv_writer_is_byte_identical(tmp_path, threads):
+    from paper_2312_01121_b200 import _native
+
+    g = np.random.default_rng(11)
+    R, n = 7, 9000  # > one 16384-row block per thread
+    states = g.standard_normal((R, n, 3)) * 10.0 ** g.integers(-320, 300, (R, n, 3))
+    special = [0.0, -0.0, 1.0, -1.0, 1e-4, 9.9999999999999991e-05, 1e16, 1e17, 123456789012345678.0,
+               5e-324, -2.2250738585072014e-308, 1.7976931348623157e308, 0.1, 1 / 3, np.inf,
+               -np.inf, np.nan, -np.nan]
+    flat = states.reshape(-1)
+    flat[:len(special)] = special
+    times = np.arange(R) * 1e-11 * 137
+    path = tmp_path / "traj.csv"
+    _native.write_trajectory_csv(path, times, states, threads=threads)
+    assert path.read_text() == _reference_csv_text(times, states)
+
+
+def test_write_trajectory_csv_public_api(tmp_path):
+    states = np.random.default_rng(2).uniform(-1, 1, (3, 5, 3))
+    traj = sto.Trajectory(times=np.array([0.0, 1e-10, 2e-10]), states=states, max_norm_drift=0.0,
+                          config=sto.RunConfig(n=5, steps=20, dt=1e-11), elapsed_seconds=0.0)
+    sto.write_trajectory_csv(tmp_path / "a.csv", traj)
+    assert (tmp_path / "a.csv").read_text() == _reference_csv_text(traj.times, states)
