@@ -57,3 +57,14 @@ def oracle_mod():
 
     oracle.build()
     return oracle
+
+
+@pytest.fixture(scope="session")
+def spinosc_ref():
+    """The reference package itself, installed offline into baseline/_ref (git-ignored,
+    travels to the GPU box with the snapshot); tests using it skip when it is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if ref.is_dir() and str(ref) not in sys.path:
+        sys.path.append(str(ref))
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_sto")
+    return pytest.importorskip("spinosc")

@@ -1,0 +1,105 @@
+"""The B200 backend inside the reference package's own registry, integrator and CLI
+(paper_2312_01121_b200/spinosc_plugin.py).
+
+CPU: registration replaces spinosc's "gpu" entry, its probe never raises and is
+false without a GPU, and the whole-run hook leaves every other backend on the
+reference's untouched loop (bit-identical trajectories).
+GPU: `spinosc validate` passes the B200 backend against the numpy reference
+(deviation 0.0), `spinosc.integrate(..., backend="gpu")` runs in one launch and
+matches the reference's `fused` backend bit for bit, divergence surfaces as the
+reference's IntegrationDivergedError, and `spinosc bench` reports its speedup.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+
+@pytest.fixture(scope="module")
+def plugged(spinosc_ref):
+    from paper_2312_01121_b200 import spinosc_plugin
+
+    spinosc_plugin.register()
+    spinosc_plugin.register()  # idempotent
+    return spinosc_ref
+
+
+def test_registered_under_reference_id(plugged):
+    desc = {d.backend_id: d for d in plugged.list_backends()}
+    assert desc["gpu"].kind.startswith("B200")
+    import spinosc.integrator as integ
+
+    assert getattr(integ.integrate, "__wrapped__", None) is not None
+    import spinosc.cli as cli
+
+    assert cli.integrate is integ.integrate
+
+
+def test_probe_never_raises(plugged):
+    from paper_2312_01121_b200 import spinosc_plugin
+
+    assert spinosc_plugin._probe() in (True, False)
+
+
+def test_hook_keeps_reference_loop_for_cpu_backends(plugged):
+    sp = plugged
+    top = sp.build_topology(12, seed=3)
+    cfg = sp.RunConfig(n=12, steps=40, dt=1e-11, record_stride=10, backend="reference")
+    import spinosc.integrator as integ
+
+    a = integ.integrate(top, sp.PhysicalParams(), cfg)
+    b = integ.integrate.__wrapped__(top, sp.PhysicalParams(), cfg)
+    assert np.array_equal(a.states, b.states) and np.array_equal(a.times, b.times)
+
+
+@pytest.mark.gpu
+def test_reference_validate_passes_b200(plugged, capsys):
+    import spinosc.cli as cli
+
+    rc = cli.main(["validate", "--n", "100", "--steps", "1000", "--record-stride", "100"])
+    out = capsys.readouterr().out
+    assert rc == 0, out
+    line = next(l for l in out.splitlines() if "vs gpu" in l)
+    assert "max deviation 0.000e+00" in line and "PASS" in line
+
+
+@pytest.mark.gpu
+def test_reference_integrate_whole_run_bit_exact(plugged):
+    sp = plugged
+    top = sp.build_topology(300, seed=1)
+    series = sp.InputSeries(np.random.default_rng(2).uniform(-1, 1, (100, 1)), 5)
+    cfg = sp.RunConfig(n=300, steps=500, dt=1e-11, record_stride=50, input_series=series,
+                       backend="gpu")
+    g = sp.integrate(top, sp.PhysicalParams(), cfg)
+    f = sp.integrate(top, sp.PhysicalParams(), cfg.with_overrides(backend="fused"))
+    assert type(g) is type(f)
+    assert np.array_equal(g.states.view(np.uint64), f.states.view(np.uint64))
+    assert np.array_equal(g.times, f.times) and g.max_norm_drift == f.max_norm_drift
+
+
+@pytest.mark.gpu
+def test_reference_divergence_error(plugged):
+    sp = plugged
+    params = sp.PhysicalParams().with_overrides(h_appl=1e300)
+    cfg = sp.RunConfig(n=4, steps=30, dt=1e-11, record_stride=10, backend="gpu")
+    with pytest.raises(sp.IntegrationDivergedError) as info:
+        sp.integrate(sp.Topology.decoupled(4), params, cfg)
+    want = None
+    try:
+        sp.integrate(sp.Topology.decoupled(4), params, cfg.with_overrides(backend="reference"))
+    except sp.IntegrationDivergedError as exc:
+        want = exc
+    assert want is not None
+    assert (info.value.oscillator, info.value.step) == (want.oscillator, want.step)
+
+
+@pytest.mark.gpu
+def test_reference_bench_lists_b200(plugged, capsys):
+    import spinosc.cli as cli
+
+    rc = cli.main(["bench", "--n-list", "10,100", "--steps", "500", "--backends",
+                   "reference,gpu", "--repetitions", "1"])
+    out = capsys.readouterr().out
+    assert rc == 0, out
+    assert "gpu n=100:" in out
