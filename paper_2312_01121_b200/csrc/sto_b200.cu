@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/sto.h"
@@ -139,20 +141,51 @@ struct Layout {
     double *w = nullptr;
 };
 
+// Big buffers (the W layout, its staging copy) come from the device's
+// stream-ordered pool with an unbounded release threshold, so destroying a
+// plan and building the next one (the e2e path: one plan per integrate())
+// reuses the memory instead of paying cudaMalloc/cudaFree of ~1 GB each time.
+void keep_pool_memory() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+}
+
+bool is_device_pointer(const void *p) {
+    cudaPointerAttributes attr;
+    int dev = -1;
+    const bool ok = cudaPointerGetAttributes(&attr, p) == cudaSuccess && cudaGetDevice(&dev) == cudaSuccess &&
+                    (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) &&
+                    attr.device == dev;
+    cudaGetLastError();
+    return ok;
+}
+
 int upload_layout(Layout &L, int rows, int cols, const double *a, long long lda, int blk_hint,
                   cudaStream_t stream) {
     L.rows = rows;
     L.cs = make_sched(cols, blk_hint);
+    keep_pool_memory();
     const size_t bytes = (size_t)rows * L.cs.ldw * sizeof(double);
-    STO_CUDA(cudaMalloc(&L.w, bytes));
-    double *stage = nullptr;
-    STO_CUDA(cudaMalloc(&stage, (size_t)rows * cols * sizeof(double)));
-    STO_CUDA(cudaMemcpy2DAsync(stage, (size_t)cols * sizeof(double), a, (size_t)lda * sizeof(double),
-                               (size_t)cols * sizeof(double), rows, cudaMemcpyDefault, stream));
-    permute_rows_kernel<<<1184, 256, 0, stream>>>(stage, cols, L.w, rows, L.cs);
-    STO_CUDA(cudaGetLastError());
+    STO_CUDA(cudaMallocAsync(&L.w, bytes, stream));
+    if (is_device_pointer(a)) {  // device-built W: permute in place, no staging copy
+        permute_rows_kernel<<<1184, 256, 0, stream>>>(a, lda, L.w, rows, L.cs);
+        STO_CUDA(cudaGetLastError());
+    } else {
+        double *stage = nullptr;
+        STO_CUDA(cudaMallocAsync(&stage, (size_t)rows * cols * sizeof(double), stream));
+        STO_CUDA(cudaMemcpy2DAsync(stage, (size_t)cols * sizeof(double), a, (size_t)lda * sizeof(double),
+                                   (size_t)cols * sizeof(double), rows, cudaMemcpyDefault, stream));
+        permute_rows_kernel<<<1184, 256, 0, stream>>>(stage, cols, L.w, rows, L.cs);
+        STO_CUDA(cudaGetLastError());
+        STO_CUDA(cudaFreeAsync(stage, stream));
+    }
     STO_CUDA(cudaStreamSynchronize(stream));
-    STO_CUDA(cudaFree(stage));
     return STO_OK;
 }
 
@@ -327,7 +360,19 @@ int check_device(int device, cudaDeviceProp *prop) {
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count)
         return fail(STO_E_UNAVAILABLE, "no CUDA device " + std::to_string(device));
-    STO_CUDA(cudaGetDeviceProperties(prop, device));
+    // properties cached per device (cudaGetDeviceProperties costs ~8 ms per call)
+    static std::mutex mu;
+    static std::map<int, cudaDeviceProp> cache;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(device);
+        if (it == cache.end()) {
+            cudaDeviceProp p;
+            STO_CUDA(cudaGetDeviceProperties(&p, device));
+            it = cache.emplace(device, p).first;
+        }
+        *prop = it->second;
+    }
     if (prop->major != 10)
         return fail(STO_E_UNAVAILABLE, std::string("device is not sm_100-class: ") + prop->name);
     return STO_OK;
@@ -342,11 +387,11 @@ const char *sto_last_error(void) { return g_err.c_str(); }
 int sto_abi_version(void) { return STO_ABI_VERSION; }
 
 int sto_probe(int device) {
-    cudaDeviceProp prop;
-    int count = 0;
+    int count = 0, major = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) return 0;
-    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return 0;
-    return prop.major == 10 ? 1 : 0;
+    // one attribute query (cudaGetDeviceProperties costs ~8 ms per call)
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess) return 0;
+    return major == 10 ? 1 : 0;
 }
 
 int64_t sto_n_records(int64_t steps, int64_t record_stride) {
@@ -507,10 +552,11 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
 void sto_plan_destroy(sto_plan *P) {
     if (!P) return;
     cudaSetDevice(P->device);
+    cudaDeviceSynchronize();  // no launch may still read the plan's buffers
     for (int q = 0; q < kMaxRanks; ++q)
         if (P->ipc_opened[q]) cudaIpcCloseMemHandle(P->ipc_opened[q]);
     cudaFree(P->exch);
-    cudaFree(P->L.w);
+    cudaFreeAsync(P->L.w, nullptr);
     cudaFree(P->w_in);
     cudaFree(P->xbuf);
     cudaFree(P->bar);
@@ -953,7 +999,8 @@ int sto_tree_matvec(int device, int64_t rows, int64_t cols, const double *a, int
     }
     cudaFree(dx);
     cudaFree(dout);
-    cudaFree(L.w);
+    cudaDeviceSynchronize();
+    cudaFreeAsync(L.w, nullptr);
     return rc;
 }
 
