@@ -68,6 +68,9 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+RK4_CHAIN_CYCLES = 1125  # profiles/r01_microbench.json "rk4_step_cyc"
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -486,11 +489,26 @@ def run_ours(args, rank, world, local_rank):
     peaks = measured_peaks()
     alg_bytes = 32.0 * rows_mine * n * steps  # one f64 W row per RK stage per (own) osc-step
     achieved = alg_bytes / kernel_s / 1e9
+    kname = {"tiny": "tiny_rk4_kernel", "reg": "reg_rk4_kernel", "single": "grid_rk4_kernel[Shared,single]",
+             "resident": "grid_rk4_kernel[Shared]",
+             "stream": "grid_rk4_kernel[GlobalStream]"}.get(info["kernel_name"], info["kernel_name"])
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                 "traffic": traffic_per_launch(name, steps),
                 "peak_source": "fallback" if peaks.get("fallback") else "measured",
-                "kernel": f"grid_rk4_kernel[{info['kernel_name']}]"}
+                "kernel": kname}
+    if n < 1000:
+        # W is a few KB: no HBM/tensor roofline applies.  The bound is the dependent
+        # fp64 chain of one RK4 step (4 RHS evaluations, DDIV included): 1125 cycles
+        # measured by tools/microbench.cu (profiles/r01_microbench.json).
+        clk = clocks.summary().get("sm_mhz") or 1965.0
+        peak_steps = clk * 1e6 / RK4_CHAIN_CYCLES
+        got = steps / kernel_s
+        roofline = {"bound": "latency", "achieved": got, "peak": peak_steps, "unit": "RK4 steps/s",
+                    "frac": got / peak_steps, "traffic": None,
+                    "peak_source": f"measured dependent-chain bound ({RK4_CHAIN_CYCLES} cycles per RK4 "
+                                   f"step at {clk:.0f} MHz, tools/microbench.cu)",
+                    "kernel": kname}
 
     # ----------------------------------------------------- cpu baseline ----
     cpu = None
