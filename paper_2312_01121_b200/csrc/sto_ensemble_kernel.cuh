@@ -182,6 +182,31 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// The RHS of model.py:239-301 with FMA contraction and a correctly rounded
+// reciprocal instead of the pinned separately-rounded order: ~45 % fewer FP64
+// instructions and a shorter dependent chain for the epilogue, which shares
+// the FP64 datapath with the DMMAs of the other warp group.  Same algebra;
+// differences are at the rounding level, inside the ensemble's GEMM-order
+// tolerance (tests/test_gpu_ensemble.py holds every member to 1e-10).
+__device__ __forceinline__ V3 row_rhs_fma(V3 m, double cp, double cin, const Consts &c) {
+    const double md = fma(m.z, c.pz, fma(m.y, c.py, m.x * c.px));
+    const double hs = c.pref * __drcp_rn(fma(c.lam, md, 1.0));
+    const double qx = fma(c.py, m.z, -(c.pz * m.y));
+    const double qy = fma(c.pz, m.x, -(c.px * m.z));
+    const double qz = fma(c.px, m.y, -(c.py * m.x));
+    const double bx = fma(hs, qx, fma(c.a_cp, cp, c.a_in * cin));
+    const double by = hs * qy;
+    const double bz = fma(hs, qz, fma(c.h_aniso, m.z, c.h_appl));
+    const double ax = fma(m.y, bz, -(m.z * by));
+    const double ay = fma(m.z, bx, -(m.x * bz));
+    const double az = fma(m.x, by, -(m.y * bx));
+    const double ex = fma(m.y, az, -(m.z * ay));
+    const double ey = fma(m.z, ax, -(m.x * az));
+    const double ez = fma(m.x, ay, -(m.y * ax));
+    return V3{fma(-c.c_prec, ax, -(c.c_damp * ex)), fma(-c.c_prec, ay, -(c.c_damp * ey)),
+              fma(-c.c_prec, az, -(c.c_damp * ez))};
+}
+
 #ifdef STO_TIMELINE
 __device__ unsigned long long g_ens_timeline[16][8];  // [stage][event + 4 * group]
 #define ENS_TL(e, ev)                                                                         \
@@ -521,7 +546,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
                         cin = p.st[(size_t)k * p.bp + bg];
                     }
                 }
-                const V3 d = row_rhs(cur, cpb[rl * kEnsLDB + bl], cin, c);
+                const V3 d = row_rhs_fma(cur, cpb[rl * kEnsLDB + bl], cin, c);
                 double xpub;
                 if (stage < 3) {
                     // acc: k1 | k1 + k2*2 | (k1 + k2*2) + k3*2
