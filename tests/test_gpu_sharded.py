@@ -73,3 +73,29 @@ def test_group_divergence_is_consistent():
         integrate_logical(top, sto.PhysicalParams(), sto.initial_state(n), drive, 5, 1e-11, 100,
                           10, world=3)
     assert info.value.step == 60
+
+
+@pytest.mark.parametrize("world,n", [(2, 1500), (4, 3000)])
+def test_ipc_transport_multiprocess(world, n):
+    """The real multi-process transport (CUDA-IPC handle exchange over
+    torch.distributed, peer stores into every rank's receive buffer,
+    st.release.sys epoch flags, epochs carried across runs): `world` processes
+    on ONE GPU via torchrun, bit-exact against the oracle (tools/ipc_selftest.py)."""
+    import json
+    import socket
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node",
+           str(world), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(ROOT / "tools" / "ipc_selftest.py"), str(n), "2"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert out.returncode == 0 and lines, out.stdout[-2000:] + out.stderr[-2000:]
+    res = json.loads(lines[-1])
+    assert res["ok"] and res["world"] == world, res
