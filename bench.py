@@ -204,6 +204,15 @@ def best_threads(top, name: str, sample: int) -> int:
     return 1 if t_one < t_all else cores
 
 
+def gpu_and_backend(local_rank: int):
+    """One process per GPU over NCCL.  STO_BENCH_SHARE_GPU=1 (tests only) puts every
+    rank on cuda:0 with gloo, so the multi-rank code path (IPC handle exchange,
+    in-kernel all-gather, max-over-ranks timing) runs on a one-GPU box."""
+    if os.environ.get("STO_BENCH_SHARE_GPU") == "1":
+        return 0, "gloo"
+    return local_rank, "nccl"
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -256,13 +265,16 @@ def run_ours_ensemble(args, rank, world, local_rank):
     import paper_2312_01121_b200 as sto
     from paper_2312_01121_b200.backends.b200 import B200Backend
 
-    dev = local_rank
+    dev, backend_name = gpu_and_backend(local_rank)
     torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if backend_name == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend_name)
     name = args.workload
     n, steps, desc, _ = WORKLOADS[name]
     if args.rk4_steps:
@@ -371,13 +383,16 @@ def run_ours(args, rank, world, local_rank):
     from paper_2312_01121_b200 import _native
     from paper_2312_01121_b200.backends.b200 import B200Backend
 
-    dev = local_rank
+    dev, backend_name = gpu_and_backend(local_rank)
     torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if backend_name == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend_name)
 
     name = args.workload
     n, steps, desc, _ = WORKLOADS[name]

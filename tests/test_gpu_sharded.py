@@ -99,3 +99,29 @@ def test_ipc_transport_multiprocess(world, n):
     assert out.returncode == 0 and lines, out.stdout[-2000:] + out.stderr[-2000:]
     res = json.loads(lines[-1])
     assert res["ok"] and res["world"] == world, res
+
+
+def test_bench_multirank_path_on_one_gpu():
+    """bench.py --gpus 2 under torchrun (STO_BENCH_SHARE_GPU: both ranks on cuda:0,
+    gloo): the row-sharded n1e4 path -- ShardedB200Backend construction, IPC
+    connect, timed runs, max-over-ranks, e2e -- prints one valid JSON line."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, STO_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--rk4-steps", "4", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert out.returncode == 0 and len(lines) == 1, out.stdout[-2000:] + out.stderr[-3000:]
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and "row-sharded" in line["config"]["parallelism"]
