@@ -209,6 +209,7 @@ struct sto_plan {
     // integrate launch configuration
     int kind = kStream;
     bool stream_evict_first = true;
+    int l2_keep_rows = 0;             // streaming kernel: rows per CTA kept L2-resident
     int grid = 1;
     int rows_cap = 1;
     int chunk_cols = 0;
@@ -337,6 +338,19 @@ int launch_tiny(const KParams &p, int n, cudaStream_t stream) {
     return STO_OK;
 }
 
+// Streaming W (> 0.6 L2): a fixed slice of every CTA's rows is loaded with
+// evict_last and stays L2-resident across stages, so each stage reads that
+// slice from L2 and only the rest from HBM.  Budget: kL2KeepFrac of L2
+// (STO_L2_KEEP_MB overrides, 0 disables), spread evenly over the CTAs so the
+// per-stage work stays balanced.
+constexpr double kL2KeepFrac = 0.5;
+int l2_keep_rows_for(int l2_bytes, int ctas, int ldw) {
+    double budget = kL2KeepFrac * (double)l2_bytes;
+    if (const char *e = getenv("STO_L2_KEEP_MB")) budget = atof(e) * 1048576.0;
+    const double row_bytes = (double)ldw * sizeof(double);
+    return std::max(0, (int)(budget / (row_bytes * std::max(1, ctas))));
+}
+
 KParams base_params(const sto_plan *P) {
     KParams p{};
     p.cs = P->L.cs;
@@ -348,6 +362,7 @@ KParams base_params(const sto_plan *P) {
     p.xbuf = P->xbuf;
     p.bar = P->bar;
     p.status = P->status;
+    p.l2_keep_rows = P->l2_keep_rows;
     p.x_stride = 1;
     p.n_samples = 1;
     p.sps = 1;
@@ -481,6 +496,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
             P->smem = grid_smem(P->rows_cap, cs, P->chunk_cols, false);
             const double wbytes = (double)P->rows * cs.ldw * sizeof(double);
             P->stream_evict_first = wbytes > 0.6 * (double)P->l2_bytes;
+            if (P->stream_evict_first) P->l2_keep_rows = l2_keep_rows_for(P->l2_bytes, g, cs.ldw);
         }
         P->grid = g;
     } else if (n <= 32 && !(fl & STO_PLAN_NO_TINY) && !forced) {
@@ -542,6 +558,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
             P->smem = grid_smem(P->rows_cap, cs, P->chunk_cols, false);
             const double wbytes = (double)n * cs.ldw * sizeof(double);
             P->stream_evict_first = wbytes > 0.6 * (double)P->l2_bytes;
+            if (P->stream_evict_first) P->l2_keep_rows = l2_keep_rows_for(P->l2_bytes, g, cs.ldw);
         }
         P->grid = g;
     }

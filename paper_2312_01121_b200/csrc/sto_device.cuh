@@ -211,12 +211,14 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
     return pol;
 }
 
+// `pol` is the L2 cache-hint policy of this row (global sources): the streaming
+// kernel keeps a slice of W L2-resident (evict_last) and streams the rest
+// (evict_first); see KParams::l2_keep_rows.
 template <WSrc S>
-__device__ __forceinline__ double2 load_w2(const double *p) {
+__device__ __forceinline__ double2 load_w2(const double *p, uint64_t pol) {
     if constexpr (S == WSrc::Shared) {
         return *reinterpret_cast<const double2 *>(p);
     } else {
-        const uint64_t pol = (S == WSrc::GlobalL2) ? l2_policy_evict_last() : l2_policy_evict_first();
         double2 v;
         asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                      : "=d"(v.x), "=d"(v.y)
@@ -228,11 +230,12 @@ __device__ __forceinline__ double2 load_w2(const double *p) {
 // Node of one segment (32*C columns).  wseg/xseg point at the segment start
 // of the W row and of the staged X vector (same layout).
 template <int C, WSrc S>
-__device__ __forceinline__ double segment_node(const double *wseg, const double *xseg, int lane) {
+__device__ __forceinline__ double segment_node(const double *wseg, const double *xseg, int lane,
+                                               uint64_t pol) {
     double p[C];
 #pragma unroll
     for (int i = 0; i < C / 2; ++i) {
-        const double2 w = load_w2<S>(wseg + ((i << 5) + lane) * 2);
+        const double2 w = load_w2<S>(wseg + ((i << 5) + lane) * 2, pol);
         const double2 x = *reinterpret_cast<const double2 *>(xseg + ((i << 5) + lane) * 2);
         p[2 * i] = rmul(w.x, x.x);
         p[2 * i + 1] = rmul(w.y, x.y);
@@ -250,11 +253,11 @@ __device__ __forceinline__ double segment_node(const double *wseg, const double 
 
 template <WSrc S>
 __device__ __forceinline__ double tail_segment_node(int c, const double *wseg, const double *xseg,
-                                                    int lane) {
+                                                    int lane, uint64_t pol) {
     switch (c) {
-        case 8: return segment_node<8, S>(wseg, xseg, lane);
-        case 4: return segment_node<4, S>(wseg, xseg, lane);
-        default: return segment_node<2, S>(wseg, xseg, lane);
+        case 8: return segment_node<8, S>(wseg, xseg, lane, pol);
+        case 4: return segment_node<4, S>(wseg, xseg, lane, pol);
+        default: return segment_node<2, S>(wseg, xseg, lane, pol);
     }
 }
 
@@ -266,7 +269,7 @@ __device__ __forceinline__ double tail_segment_node(int c, const double *wseg, c
 // physical column held in the X window).
 template <WSrc S>
 __device__ __forceinline__ double block_node(const ColSched &cs, int b, const double *wrow,
-                                             const double *xwin, int x_base, int lane) {
+                                             const double *xwin, int x_base, int lane, uint64_t pol) {
     const int c0 = b * cs.blk;
     const int seg0 = c0 / kSegFull;
     const int per = cs.blk / kSegFull;
@@ -279,7 +282,7 @@ __device__ __forceinline__ double block_node(const ColSched &cs, int b, const do
     for (int j = 0; j < kMaxLeaves; ++j) {
         if (j < nf) {
             const int col = (seg0 + j) * kSegFull;
-            leaf[j] = segment_node<16, S>(wrow + col, xwin + (col - x_base), lane);
+            leaf[j] = segment_node<16, S>(wrow + col, xwin + (col - x_base), lane, pol);
         }
     }
     int width = nf;
@@ -287,7 +290,7 @@ __device__ __forceinline__ double block_node(const ColSched &cs, int b, const do
         double t = 0.0;
         for (int k = cs.ntail - 1; k >= 0; --k) {
             const int col = cs.tail_base[k];
-            const double v = tail_segment_node<S>(cs.tail_c[k], wrow + col, xwin + (col - x_base), lane);
+            const double v = tail_segment_node<S>(cs.tail_c[k], wrow + col, xwin + (col - x_base), lane, pol);
             t = (k == cs.ntail - 1) ? v : radd(v, t);
         }
 #pragma unroll

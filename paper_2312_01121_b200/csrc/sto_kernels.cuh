@@ -94,6 +94,8 @@ struct KParams {
     double *xbuf;           // 2 x ldw published stage x (physical layout), +0.0 padded
     unsigned long long *bar;
     StatusDev *status;
+    int l2_keep_rows;       // GlobalStream: each CTA's first l2_keep_rows rows load with
+                            // evict_last (stay L2-resident across stages), the rest evict_first
     MultiParams mp;         // MULTI only
 };
 
@@ -242,6 +244,8 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
     const int blocks_per_chunk = p.chunk_cols >= cs.ldw ? cs.nblocks : p.chunk_cols / cs.blk;
     const double *u = p.samples;
 
+    const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
+    const int keep_rows = (S == WSrc::GlobalL2) ? nrow : (S == WSrc::GlobalStream ? p.l2_keep_rows : 0);
     for (long long e = 0; e < total_stages; ++e) {
         const int stage = (int)(e & 3);
         const long long step = (e >> 2) + 1;
@@ -278,7 +282,8 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
                 const int bb = bfirst + unit % bcount;
                 const double *wrow = (S == WSrc::Shared) ? wres + (size_t)r * cs.ldw
                                                          : Wg + (size_t)(r0 + r) * cs.ldw;
-                const double node = block_node<S>(cs, bb, wrow, xs, x_base, lane);
+                const double node = block_node<S>(cs, bb, wrow, xs, x_base, lane,
+                                                  r < keep_rows ? pol_last : pol_first);
                 if (lane == 0) nodes[(size_t)r * cs.nblocks + bb] = node;
             }
             __syncthreads();
