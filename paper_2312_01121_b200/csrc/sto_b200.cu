@@ -495,7 +495,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
             P->chunk_cols = choose_chunk(cs, P->rows_cap, false);
             P->smem = grid_smem(P->rows_cap, cs, P->chunk_cols, false);
             const double wbytes = (double)P->rows * cs.ldw * sizeof(double);
-            P->stream_evict_first = wbytes > 0.6 * (double)P->l2_bytes;
+            P->stream_evict_first = wbytes > 0.75 * (double)P->l2_bytes;
             if (P->stream_evict_first) P->l2_keep_rows = l2_keep_rows_for(P->l2_bytes, g, cs.ldw);
         }
         P->grid = g;
@@ -557,7 +557,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
             P->chunk_cols = choose_chunk(cs, P->rows_cap, false);
             P->smem = grid_smem(P->rows_cap, cs, P->chunk_cols, false);
             const double wbytes = (double)n * cs.ldw * sizeof(double);
-            P->stream_evict_first = wbytes > 0.6 * (double)P->l2_bytes;
+            P->stream_evict_first = wbytes > 0.75 * (double)P->l2_bytes;
             if (P->stream_evict_first) P->l2_keep_rows = l2_keep_rows_for(P->l2_bytes, g, cs.ldw);
         }
         P->grid = g;
