@@ -364,7 +364,7 @@ def run_ours_ensemble(args, rank, world, local_rank):
             "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_TENSOR_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_TENSOR_PEAK_TFLOPS,
-                         "traffic": None,
+                         "traffic": traffic_per_launch("ens512", steps),
                          "peak_source": "measured here: DMMA f64 microbenchmark (tools/fp64_peak.cu)",
                          "kernel": "ens_rk4_kernel"},
             "cpu_baseline": cpu,
@@ -520,7 +520,7 @@ def run_ours(args, rank, world, local_rank):
         peak_steps = clk * 1e6 / RK4_CHAIN_CYCLES
         got = steps / kernel_s
         roofline = {"bound": "latency", "achieved": got, "peak": peak_steps, "unit": "RK4 steps/s",
-                    "frac": got / peak_steps, "traffic": None,
+                    "frac": got / peak_steps, "traffic": traffic_per_launch(name, steps),
                     "peak_source": f"measured dependent-chain bound ({RK4_CHAIN_CYCLES} cycles per RK4 "
                                    f"step at {clk:.0f} MHz, tools/microbench.cu)",
                     "kernel": kname}
