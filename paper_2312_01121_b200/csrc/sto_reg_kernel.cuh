@@ -130,19 +130,23 @@ __global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __
     if (threadIdx.x == 0) *sstop = 0;
     __syncthreads();
 
-    const double *u = p.samples;
     long long next_rec = p.stride;
     long long rec_idx = 1;
     unsigned epoch = 0;
     bool stop = false;
     RhsPre pre{};
+    // input field of step `st` (zero-order hold, model.py:93-149)
+    auto cin_of = [&](long long st) {
+        const double *us = p.n_samples > 1 ? p.samples + ((st - 1) / p.sps) * p.n_in : p.samples;
+        return (p.n_in == 1) ? rmul(p.w_in[k], us[0]) : tree_dot_stream(p.w_in + (size_t)k * p.n_in, us, p.n_in);
+    };
+    double cin = 0.0;
+    if (!SINGLE && owner) {  // step 1; later steps prepare cin and stage 0's own-state half
+        cin = cin_of(1);     // during the previous step's last exchange
+        pre = row_rhs_pre(m, cin, p.c);
+    }
     for (long long step = 1; step <= p.steps && !stop; ++step) {
-        double cin = 0.0;
-        if (owner) {
-            cin = (p.n_in == 1) ? rmul(p.w_in[k], u[0])
-                                : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
-            if (!SINGLE) pre = row_rhs_pre(m, cin, p.c);  // own-state half for stage 0
-        }
+        if (SINGLE && owner) cin = cin_of(step);
         const bool record = (step == next_rec) || (step == p.steps);
 #pragma unroll 1
         for (int stage = 0; stage < 4; ++stage) {
@@ -227,13 +231,8 @@ __global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __
                 if (*sstop) stop = true;
             } else {
                 ++epoch;
-                if (owner) {
-                    st_ll(rp.ll + (size_t)(epoch & 1) * n + k, xpub,
-                          epoch | (bad ? 0x80000000u : 0u));
-                    // next stage's own-state half, off the critical path: the
-                    // exchange below takes an L2 round trip anyway
-                    if (stage < 3) pre = row_rhs_pre(s, cin, p.c);
-                }
+                if (owner)
+                    st_ll(rp.ll + (size_t)(epoch & 1) * n + k, xpub, epoch | (bad ? 0x80000000u : 0u));
                 TL(estage, 2);
                 if (!last) {
                     const uint4 *slot = rp.ll + (size_t)(epoch & 1) * n;
@@ -242,10 +241,25 @@ __global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __
                     for (int q = 0; q < kLLMaxPerThread; ++q)
                         if (threadIdx.x + q * blockDim.x < n) pending |= 1u << q;
                     uint4 got[kLLMaxPerThread];
+                    bool first = true;
                     while (pending) {
 #pragma unroll
                         for (int q = 0; q < kLLMaxPerThread; ++q)
                             if (pending & (1u << q)) got[q] = ld_ll(slot + threadIdx.x + q * blockDim.x);
+                        if (first) {
+                            // next stage's own-state half (its IEEE division included) is
+                            // computed while the first round of exchange loads is in flight;
+                            // after stage 3 that is the next step's input field and stage 0
+                            if (owner) {
+                                if (stage < 3) {
+                                    pre = row_rhs_pre(s, cin, p.c);
+                                } else {
+                                    cin = cin_of(step + 1);
+                                    pre = row_rhs_pre(m, cin, p.c);
+                                }
+                            }
+                            first = false;
+                        }
 #pragma unroll
                         for (int q = 0; q < kLLMaxPerThread; ++q) {
                             if ((pending & (1u << q)) && (got[q].y & 0x7fffffffu) == epoch &&
@@ -271,7 +285,6 @@ __global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __
             next_rec += p.stride;
             ++rec_idx;
         }
-        if (p.n_samples > 1) u = p.samples + (step / p.sps) * p.n_in;
     }
     if (owner) {
         double *mm = p.m + 3 * (size_t)k;
