@@ -804,6 +804,7 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
         e.bar = P->ens_bar;
         e.status = P->status;
         e.debug_solo = getenv("STO_ENS_DEBUG_SOLO") ? 1 : 0;
+        e.gate_frac = getenv("STO_ENS_GATE") ? (float)atof(getenv("STO_ENS_GATE")) : 0.5f;
         STO_CUDA(cudaMemsetAsync(P->ens_x, 0, sizeof(double) * 2 * kp * bp, s));
         STO_CUDA(cudaMemsetAsync(P->ens_bar, 0, sizeof(unsigned long long) * 32 * 1024, s));
         const int rc = launch_ens_u(U, e, n_rt * ncols, s);

@@ -115,6 +115,7 @@ struct EnsParams {
     unsigned long long *bar;      // per half-column counters, 32 words apart
     StatusDev *status;
     int debug_solo;               // timeline experiments: group 1 idles (results of its members invalid)
+    float gate_frac;              // group 1 starts when group 0 has consumed this fraction of stage 0
 };
 
 // Fragment-order layouts.  K is cut into 32-column chunks (the last one may be
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
         ch_fill = 0;
         g_fill = 1;
     }
-    const int gate_chunk = n_chunks / 2;
+    const int gate_chunk = min(n_chunks - 1, (int)(p.gate_frac * n_chunks));
     long long next_rec = p.stride, rec_idx = 1;
     long long gstage = 0;
     for (long long step = 1; step <= (p.debug_solo && grp == 1 ? 0 : p.steps); ++step) {
