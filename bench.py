@@ -72,9 +72,19 @@ RK4_CHAIN_CYCLES = 1125  # profiles/r01_microbench.json "rk4_step_cyc"
 
 
 def measured_peaks() -> dict:
+    """Roofline denominators: the driver-written MEASURED_PEAKS.json (hbm_gbs = STREAM
+    copy on this pool's B200s), else the profiling recipe's fallback 6.65 TB/s."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
-        return json.loads(p.read_text())
+        try:
+            d = json.loads(p.read_text())
+            v = d.get("hbm_gbs")
+            if isinstance(v, dict):  # tolerate {"value": ...} entries
+                v = v.get("value")
+            if v:
+                return {"hbm_gbs": float(v), "fallback": False}
+        except Exception:
+            pass
     return {"hbm_gbs": 6650.0, "fallback": True}
 
 
