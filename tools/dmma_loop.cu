@@ -3,7 +3,13 @@
 // with its per-chunk synchronisation switched on step by step.  Finds what keeps the
 // in-kernel DMMA rate below tools/dmma_rate.cu's ceiling.
 #include <cstdio>
-constexpr int U = 7, KC = 48, NK = KC / 4, WSL = 8 * U * KC, XSL = KC * 32, RING = 3;
+#ifndef KCH
+#define KCH 48
+#endif
+#ifndef KPH
+#define KPH 3
+#endif
+constexpr int U = 7, KC = KCH, NK = KC / 4, WSL = 8 * U * KC, XSL = KC * 32, RING = 3;
 template <int MODE>  // 0 plain, 1 + syncwarp/atomic, 2 + mbarrier try_wait, 3 + double buffer off,
                      // 4 = 2 + real ring: the last warp refills the slot by bulk async copy from L2
 __global__ void __launch_bounds__(640, 1) loop(int chunks, double *out, int warps_gemm, const double *src) {
@@ -29,7 +35,7 @@ __global__ void __launch_bounds__(640, 1) loop(int chunks, double *out, int warp
     if (MODE == 4 && threadIdx.x < RING) refill(threadIdx.x, threadIdx.x);
     if (warp >= warps_gemm) return;
     unsigned ph = 0;
-    const int mu = warp & 3, kph = warp >> 2;
+    const int mu = warp & 3, kph = (warp >> 2) % KPH;
     double acc[U][2] = {};
     int s = 0;
     for (int ch = 0; ch < chunks; ++ch) {
@@ -40,8 +46,8 @@ __global__ void __launch_bounds__(640, 1) loop(int chunks, double *out, int warp
         const double *W = sm + s * (WSL + XSL), *X = W + WSL;
         if (MODE == 3) {
 #pragma unroll
-            for (int q = 0; q < NK / 3; ++q) {
-                const int kk = 3 * q + kph;
+            for (int q = 0; q < NK / KPH; ++q) {
+                const int kk = KPH * q + kph;
                 double a[U];
 #pragma unroll
                 for (int r = 0; r < U; ++r) a[r] = W[(r * NK + kk) * 32 + lane];
@@ -57,9 +63,9 @@ __global__ void __launch_bounds__(640, 1) loop(int chunks, double *out, int warp
             for (int r = 0; r < U; ++r) a[0][r] = W[(r * NK + kph) * 32 + lane];
             bf[0] = X[(kph * 4 + mu) * 32 + lane];
 #pragma unroll
-            for (int q = 0; q < NK / 3; ++q) {
-                if (q + 1 < NK / 3) {
-                    const int kn = 3 * (q + 1) + kph;
+            for (int q = 0; q < NK / KPH; ++q) {
+                if (q + 1 < NK / KPH) {
+                    const int kn = KPH * (q + 1) + kph;
 #pragma unroll
                     for (int r = 0; r < U; ++r) a[(q + 1) & 1][r] = W[(r * NK + kn) * 32 + lane];
                     bf[(q + 1) & 1] = X[(kn * 4 + mu) * 32 + lane];
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(640, 1) loop(int chunks, double *out, int warp
         }
         if (MODE >= 1) {
             __syncwarp();
-            if (lane == 0 && atomicAdd(&done[s], 1u) % 12 == 11) {
+            if (lane == 0 && atomicAdd(&done[s], 1u) % warps_gemm == warps_gemm - 1) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 if (MODE == 4 && ch + RING < chunks) refill(s, ch + RING);
             }
@@ -102,7 +108,7 @@ void run(double *out, int sms, int threads, int gw, const double *src) {
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    const double flops = 512.0 * U * (NK / 3) * chunks * gw * sms;
+    const double flops = 512.0 * U * (NK / KPH) * chunks * gw * sms;
     printf("mode %d threads %d gemm warps %d: %.2f TFLOP/s\n", MODE, threads, gw, flops / ms / 1e9);
 }
 int main() {
@@ -113,11 +119,9 @@ int main() {
     double *src;
     cudaMalloc(&src, (size_t)200 * (WSL + XSL) * 8);
     cudaMemset(src, 0, (size_t)200 * (WSL + XSL) * 8);
-    for (int threads : {384, 640}) {
-        run<0>(out, sms, threads, 12, src);
-        run<1>(out, sms, threads, 12, src);
-        run<2>(out, sms, threads, 12, src);
-        run<4>(out, sms, threads, 12, src);
+    for (int gw : {8, 12, 16}) {
+        run<0>(out, sms, 512, gw, src);
+        run<4>(out, sms, 512, gw, src);
     }
     printf("err: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }
