@@ -1,0 +1,106 @@
+"""Property-based parity fuzzing of the CUDA path against the pinned oracle.
+
+Hypothesis draws the whole run description -- N (1 … 300, so every kernel
+family and ragged tiles/segments appear), W scale, input channels, drive
+length and hold, physical-parameter overrides, step count and recording
+stride -- and every kernel family that supports the size must reproduce the
+oracle's recorded states BIT FOR BIT (the reference's pinned order; SURVEY
+§8(c)).  A second property is the reference's own `test_derivative_is_tangent`
+(`test_model.py:111-127`) on the device derivative K0: m · dm/dt vanishes up to
+rounding.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+from conftest import assert_bit_equal
+
+pytestmark = pytest.mark.gpu
+
+FORCE = {"auto": 0, "tiny": 0, "single": 0x4 | 0x8, "resident": 0x2 | 0x8, "stream": 0x1 | 0x8,
+         "reg": 0x10 | 0x8}
+
+
+@st.composite
+def runs(draw):
+    n = draw(st.one_of(st.integers(1, 40), st.integers(41, 300)))
+    n_in = draw(st.integers(1, 3))
+    seed = draw(st.integers(0, 2**31 - 1))
+    steps = draw(st.integers(1, 60))
+    stride = draw(st.integers(1, steps))
+    sps = draw(st.integers(1, 7))
+    n_samples = -(-steps // sps)  # ceil: the reference's check_steps window
+    scale = draw(st.sampled_from([0.0, 0.3, 1.0, 3.0]))
+    over = draw(st.fixed_dictionaries({}, optional={
+        "current": st.floats(1.0e-3, 4.0e-3), "alpha": st.floats(0.002, 0.05),
+        "h_appl": st.floats(-500.0, 500.0), "a_cp": st.floats(-200.0, 200.0),
+        "a_in": st.floats(-200.0, 200.0)}))
+    return n, n_in, seed, steps, stride, sps, n_samples, scale, over
+
+
+def _families(n):
+    fams = ["auto", "stream", "resident"]
+    if n <= 1024:
+        fams.append("reg")
+    if n <= 32:
+        fams.append("tiny")
+    if n <= 128:
+        fams.append("single")
+    return fams
+
+
+@settings(max_examples=150, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(runs())
+def test_random_runs_bit_exact_every_family(oracle_mod, run):
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200.backends.b200 import B200Backend
+
+    n, n_in, seed, steps, stride, sps, n_samples, scale, over = run
+    g = np.random.default_rng(seed)
+    w = g.uniform(-1, 1, (n, n)) * (scale / np.sqrt(max(n, 1)))
+    np.fill_diagonal(w, 0.0)
+    w_in = g.uniform(-1, 1, (n, n_in))
+    samples = g.uniform(-1, 1, (n_samples, n_in))
+    params = sto.PhysicalParams().with_overrides(**over) if over else sto.PhysicalParams()
+    consts = sto.kernel_scalars(params)
+    top = sto.Topology(sto.CouplingMatrix(w), sto.InputWeights(w_in))
+    m0 = sto.initial_state(n)
+    try:
+        want, _ = oracle_mod.integrate(w, w_in, consts, m0, samples, sps, 1e-11, steps, stride)
+    except oracle_mod.OracleDiverged as exc:  # reported like the reference
+        want = exc
+    for fam in _families(n):
+        backend = B200Backend(top, params, device=0, flags=FORCE[fam])
+        m = m0.copy()
+        if isinstance(want, Exception):
+            with pytest.raises(sto.IntegrationDivergedError) as info:
+                backend.integrate_run(m, samples, sps, 1e-11, steps, stride)
+            assert (info.value.oscillator, info.value.step) == (want.oscillator, want.step)
+        else:
+            got = backend.integrate_run(m, samples, sps, 1e-11, steps, stride)
+            assert_bit_equal(got, want, f"n={n} family={fam} run={run}")
+        backend.close()
+
+
+@settings(max_examples=40, deadline=None)
+@given(seed=st.integers(min_value=0, max_value=2**31 - 1))
+def test_device_derivative_is_tangent(seed):
+    import paper_2312_01121_b200 as sto
+
+    gen = np.random.default_rng(seed)
+    n = int(gen.integers(1, 12))
+    entries = gen.uniform(-1.0, 1.0, size=(n, n))
+    np.fill_diagonal(entries, 0.0)
+    top = sto.Topology(sto.CouplingMatrix(entries),
+                       sto.InputWeights(gen.uniform(-1.0, 1.0, size=(n, 1))))
+    m = gen.standard_normal((n, 3))
+    m /= np.linalg.norm(m, axis=1, keepdims=True)
+    be = sto.create_backend("gpu", top, sto.PhysicalParams())
+    dm = np.empty_like(m)
+    be.derivative(m, gen.uniform(-1.0, 1.0, size=1), dm)
+    radial = np.abs(np.einsum("ij,ij->i", m, dm))
+    assert radial.max() <= 1e-12 * max(1.0, np.abs(dm).max())
