@@ -161,3 +161,29 @@ def test_repeat_runs_identical(sto):
     a = sto.integrate_ensemble(top, params, cfg).states
     b = sto.integrate_ensemble(top, params, cfg).states
     assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=30, deadline=None, suppress_health_check=[HealthCheck.too_slow,
+                                                                 HealthCheck.function_scoped_fixture])
+@given(n=st.integers(1, 260), batch=st.integers(1, 150), steps=st.integers(1, 80),
+       u=st.one_of(st.none(), st.integers(1, 7)), seed=st.integers(0, 2**31 - 1))
+def test_random_ensembles_within_tolerance(sto, oracle_mod, monkeypatch, n, batch, steps, u, seed):
+    """Hypothesis-drawn N, B, horizon, tile height (or the host's choice) and drive:
+    sampled members within the 1e-10 bar of the oracle."""
+    if u is None:
+        monkeypatch.delenv("STO_ENS_U", raising=False)
+    else:
+        monkeypatch.setenv("STO_ENS_U", str(u))
+    g = np.random.default_rng(seed)
+    top = _rand_top(sto, n, seed=seed)
+    params = [sto.PhysicalParams(current=c) for c in g.uniform(2.0e-3, 3.0e-3, batch)]
+    sps = int(g.integers(1, 5))
+    series = sto.InputSeries(g.uniform(-1, 1, (-(-steps // sps), 1)), sps)
+    stride = int(g.integers(1, steps + 1))
+    cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=stride, input_series=series)
+    members = sorted({0, batch - 1, int(g.integers(0, batch))})
+    _check_members(sto, oracle_mod, top, params, cfg, members)
