@@ -461,7 +461,10 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
                                 : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u, p.n_in);
     };
     input_field();
-    for (long long step = 1; step <= p.steps; ++step) {
+    // The RK4 steps run in segments that end at the next recording step or the next
+    // change of the held drive sample, so the hot loop carries no record / sample
+    // bookkeeping (a latency-bound chain: every issued instruction counts).
+    auto rk4 = [&]() {
         const V3 k1 = row_rhs(m, coupling(m.x), cin, c);
         V3 s = stage_point(m, k1, p.h2);
         publish(s.x);
@@ -475,6 +478,16 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
         const V3 k4 = row_rhs(s, coupling(s.x), cin, c);
         m = rk4_final(m, acc, k3, k4, p.dt6);
         publish(m.x);
+    };
+    long long step = 0;
+    while (step < p.steps) {
+        long long seg_end = next_rec < p.steps ? next_rec : p.steps;
+        if (p.n_samples > 1) {  // u is held for sps steps: steps step+1 .. (step/sps + 1)*sps
+            const long long hold_end = (step / p.sps + 1) * p.sps;
+            if (hold_end < seg_end) seg_end = hold_end;
+        }
+        for (long long i = step; i < seg_end; ++i) rk4();
+        step = seg_end;
         if (step == next_rec || step == p.steps) {
             const long long rec = (step == next_rec) ? rec_idx : p.n_records - 1;
             const bool bad = live && !all_finite(m);
@@ -495,7 +508,7 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
                 ++rec_idx;
             }
         }
-        if (p.n_samples > 1) {
+        if (p.n_samples > 1 && step < p.steps) {
             u = p.samples + (step / p.sps) * p.n_in;
             input_field();
         }
