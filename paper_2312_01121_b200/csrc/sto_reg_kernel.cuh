@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __
     for (long long step = 1; step <= p.steps && !stop; ++step) {
         if (SINGLE && owner) cin = cin_of(step);
         const bool record = (step == next_rec) || (step == p.steps);
-#pragma unroll 1
-        for (int stage = 0; stage < 4; ++stage) {
+#pragma unroll
+        for (int stage = 0; stage < 4; ++stage) {  // unrolled: per-stage branches resolve at compile time
             const long long estage = (step - 1) * 4 + stage;
             TL(estage, 0);
             // -------- team GEMV: pinned tree of w . x ----------------------
