@@ -415,7 +415,8 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
     for (long long step = 1; step <= (p.debug_solo && grp == 1 ? 0 : p.steps); ++step) {
         const bool record = (step == next_rec) || (step == p.steps);
         const long long sidx = p.n_samples == 1 ? 0 : (step - 1) / p.sps;
-        for (int stage = 0; stage < 4; ++stage, ++gstage) {
+#pragma unroll
+        for (int stage = 0; stage < 4; ++stage, ++gstage) {  // unrolled: stage branches resolve at compile time
             ENS_TL(gstage, 0);
             const double u1 = (p.n_in == 1) ? samp[(size_t)sidx] : 0.0;  // lands during the GEMM
             double acc[U][2];
