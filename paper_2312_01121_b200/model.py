@@ -68,6 +68,70 @@ class InputSeries:
         return self.samples[step // self.steps_per_sample]
 
 
+class Workspace:
+    """Shape tag of the reference's `Workspace` (`model.py:66-90`).
+
+    The reference preallocates host scratch (an n*n product buffer among it)
+    for its numpy derivative; here the device plan owns all scratch, so this
+    only records (n, n_in) for code that constructs and passes one around.
+    """
+
+    def __init__(self, n: int, n_in: int):
+        self.n = int(n)
+        self.n_in = int(n_in)
+
+
+def effective_field(m, params, consts=None) -> np.ndarray:
+    """(0, 0, h_appl + h_aniso m_z) per oscillator (ref `model.py:152-161`)."""
+    from .params import derive
+
+    consts = derive(params) if consts is None else consts
+    m = np.asarray(m, dtype=np.float64)
+    out = np.zeros_like(m)
+    out[:, 2] = params.h_appl + consts.h_aniso * m[:, 2]
+    return out
+
+
+def spin_torque_strength(m, params, consts=None) -> np.ndarray:
+    """h_s(m) = prefactor / (1 + lambda m.p), in Oe (ref `model.py:164-173`)."""
+    from .params import derive
+
+    consts = derive(params) if consts is None else consts
+    m = np.asarray(m, dtype=np.float64)
+    mdotp = m[:, 0] * consts.px + m[:, 1] * consts.py + m[:, 2] * consts.pz
+    return consts.h_s_prefactor / (1.0 + params.lambda_stt * mdotp)
+
+
+def coupling_field_x(coupling, m_x, a_cp: float) -> np.ndarray:
+    """a_cp (W_cp m^x) with the pinned tree on the GPU (ref `model.py:176-180`)."""
+    entries = getattr(coupling, "entries", coupling)
+    return a_cp * tree_matvec(np.asarray(entries, dtype=np.float64), np.asarray(m_x, dtype=np.float64))
+
+
+def input_field_x(weights, u, a_in: float) -> np.ndarray:
+    """a_in (W_in u) with the pinned tree on the GPU (ref `model.py:183-187`)."""
+    entries = getattr(weights, "entries", weights)
+    return a_in * tree_matvec(np.asarray(entries, dtype=np.float64), np.asarray(u, dtype=np.float64))
+
+
+def total_b(m, u, topology, params, consts=None) -> np.ndarray:
+    """Full local field b_k, shape (n, 3), same operation order as ref `model.py:190-203`."""
+    from .params import derive
+
+    consts = derive(params) if consts is None else consts
+    m = np.asarray(m, dtype=np.float64)
+    mx, my, mz = m[:, 0], m[:, 1], m[:, 2]
+    hs = spin_torque_strength(m, params, consts)
+    cpx = coupling_field_x(topology.coupling, mx, params.a_cp)
+    inx = input_field_x(topology.input_weights, np.asarray(u, dtype=np.float64), params.a_in)
+    px, py, pz = consts.px, consts.py, consts.pz
+    b = np.empty_like(m)
+    b[:, 0] = (cpx + inx) + hs * (py * mz - pz * my)
+    b[:, 1] = hs * (pz * mx - px * mz)
+    b[:, 2] = (params.h_appl + consts.h_aniso * mz) + hs * (px * my - py * mx)
+    return b
+
+
 def llg_derivative(m, u, topology, params, consts=None, out=None, workspace=None):
     """dm/dt for the whole array, evaluated by the K0 kernel on the GPU.
 

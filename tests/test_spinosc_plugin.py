@@ -106,3 +106,35 @@ def test_reference_bench_lists_b200(plugged, capsys):
     out = cap.out
     assert rc == 0, out + cap.err
     assert "gpu n=100:" in out
+
+
+def test_elementwise_field_helpers_match_reference(plugged):
+    """effective_field / spin_torque_strength: same operations as ref model.py:152-173."""
+    import paper_2312_01121_b200 as sto
+
+    g = np.random.default_rng(4)
+    m = g.standard_normal((9, 3))
+    m /= np.linalg.norm(m, axis=1, keepdims=True)
+    for over in ({}, {"current": 3.1e-3, "h_appl": -120.0}):
+        ours, ref = sto.PhysicalParams(**over), plugged.PhysicalParams(**over)
+        assert np.array_equal(sto.effective_field(m, ours), plugged.effective_field(m, ref))
+        assert np.array_equal(sto.spin_torque_strength(m, ours), plugged.spin_torque_strength(m, ref))
+
+
+@pytest.mark.gpu
+def test_total_b_matches_reference(plugged):
+    """total_b with the coupling/input sums from the device pinned tree: bit-identical
+    to the reference's numpy version (ref model.py:190-203)."""
+    import paper_2312_01121_b200 as sto
+
+    n = 37
+    top_ref = plugged.build_topology(n, n_in=2, seed=5)
+    top = sto.Topology(sto.CouplingMatrix(top_ref.coupling.entries),
+                       sto.InputWeights(top_ref.input_weights.entries))
+    g = np.random.default_rng(6)
+    m = g.standard_normal((n, 3))
+    m /= np.linalg.norm(m, axis=1, keepdims=True)
+    u = g.uniform(-1, 1, 2)
+    got = sto.total_b(m, u, top, sto.PhysicalParams())
+    want = plugged.total_b(m, u, top_ref, plugged.PhysicalParams())
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
