@@ -185,6 +185,20 @@ struct RowState {
 };
 enum { kSlotM = 0, kSlotS = 1, kSlotAcc = 2, kSlotK3 = 3 };
 
+#ifdef STO_TIMELINE
+// debug build (tools/grid_timeline.py): clock64 stamps of CTA 0 thread 0 for
+// stages [100, 116): 0 stage start, 1 x staged, 2 block phase done, 3 row phase
+// done, 4 barrier passed
+__device__ unsigned long long g_grid_timeline[16][5];
+#define GTL(e, ev)                                                                   \
+    do {                                                                             \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (e) >= 100 && (e) < 116)          \
+            g_grid_timeline[(e) - 100][ev] = clock64();                              \
+    } while (0)
+#else
+#define GTL(e, ev)
+#endif
+
 // Shared layout: [X window | W rows (resident) | nodes | row state | flags]
 template <WSrc S, bool SINGLE, bool MULTI = false>
 __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant__ KParams p) {
@@ -249,6 +263,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
     for (long long e = 0; e < total_stages; ++e) {
         const int stage = (int)(e & 3);
         const long long step = (e >> 2) + 1;
+        GTL(e, 0);
         // ---------------- block phase: tree nodes of W . x ----------------
         for (int ch = 0; ch < nchunks; ++ch) {
             const int x_base = ch * p.chunk_cols;
@@ -274,12 +289,15 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
                 }
                 __syncthreads();
             }
+            if (ch == 0) GTL(e, 1);
             const int bfirst = ch * blocks_per_chunk;
             const int bcount = min(blocks_per_chunk, cs.nblocks - bfirst);
             const int units = nrow * bcount;
             for (int unit = warp; unit < units; unit += nwarps) {
+                // blocks rotate with the row, so the (slower) tail block of consecutive
+                // rows lands on different warps instead of always the same ones
                 const int r = unit / bcount;
-                const int bb = bfirst + unit % bcount;
+                const int bb = bfirst + (unit + r) % bcount;
                 const double *wrow = (S == WSrc::Shared) ? wres + (size_t)r * cs.ldw
                                                          : Wg + (size_t)(r0 + r) * cs.ldw;
                 const double node = block_node<S>(cs, bb, wrow, xs, x_base, lane,
@@ -288,6 +306,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
             }
             __syncthreads();
         }
+        GTL(e, 2);
         // ---------------- row phase: RHS + RK4 stage update ----------------
         const long long rec = (integrate && stage == 3)
                                   ? record_index(step, p.stride, p.steps, p.n_records)
@@ -356,6 +375,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
                 xnext[col_perm(cs, k)] = xpub;
             }
         }
+        GTL(e, 3);
         if (!integrate) break;
         // MULTI also synchronises after the last stage, so that no rank can start
         // its next run (and write into a peer's buffer) while a peer still reads
@@ -377,6 +397,7 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
                 if (*sflag) break;
             }
         }
+        GTL(e, 4);
         if (stage == 3) {
             // next step's drive sample (zero-order hold, integrator.py:172)
             const long long nxt = step;  // 0-based index of the next step
