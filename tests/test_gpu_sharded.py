@@ -125,3 +125,38 @@ def test_bench_multirank_path_on_one_gpu():
     assert out.returncode == 0 and len(lines) == 1, out.stdout[-2000:] + out.stderr[-3000:]
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["value"] > 0 and "row-sharded" in line["config"]["parallelism"]
+
+
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow,
+                                                                 HealthCheck.function_scoped_fixture])
+@given(n=st.integers(8, 2500), world=st.integers(2, 8), steps=st.integers(1, 30),
+       sps=st.integers(1, 5), fam=st.sampled_from([0, 0x1, 0x2 | 0x8]),
+       seed=st.integers(0, 2**31 - 1))
+def test_random_logical_rank_runs_bit_exact(oracle_mod, n, world, steps, sps, fam, seed):
+    """Hypothesis-drawn sharded runs (world 2-8 logical ranks, ragged shards, held
+    drives, streaming / SMEM-resident families): bit-exact vs the oracle."""
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200.sharding import integrate_logical
+
+    if n < world:
+        return
+    g = np.random.default_rng(seed)
+    w = g.uniform(-1, 1, (n, n)) / np.sqrt(n / 3.0)
+    np.fill_diagonal(w, 0.0)
+    top = sto.Topology(sto.CouplingMatrix(w), sto.InputWeights(g.uniform(-1, 1, (n, 1))))
+    stride = int(g.integers(1, steps + 1))
+    samples = g.uniform(-1, 1, (-(-steps // sps), 1))
+    consts = sto.kernel_scalars(sto.PhysicalParams())
+    want, _ = oracle_mod.integrate(w, top.input_weights.entries, consts, sto.initial_state(n),
+                                   samples, sps, 1e-11, steps, stride)
+    m = sto.initial_state(n)
+    try:
+        got = integrate_logical(top, sto.PhysicalParams(), m, samples, sps, 1e-11, steps, stride,
+                                world, flags=fam)
+    except sto.ParameterError:
+        return  # family does not fit this shard (e.g. SMEM-resident rows too wide)
+    assert_bit_equal(got, want, f"n={n} world={world} fam={fam}")
