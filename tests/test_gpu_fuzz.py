@@ -31,7 +31,7 @@ def runs(draw):
     n_in = draw(st.integers(1, 3))
     seed = draw(st.integers(0, 2**31 - 1))
     steps = draw(st.integers(1, 60))
-    stride = draw(st.integers(1, steps))
+    stride = draw(st.integers(1, steps + 5))  # > steps: only the initial and final records
     sps = draw(st.integers(1, 7))
     n_samples = -(-steps // sps)  # ceil: the reference's check_steps window
     scale = draw(st.sampled_from([0.0, 0.3, 1.0, 3.0]))
