@@ -1027,6 +1027,10 @@ STO_API int sto_debug_ens_timeline(unsigned long long *out, int count) {
     STO_CUDA(cudaMemcpyFromSymbol(out, g_ens_timeline, sizeof(unsigned long long) * count));
     return STO_OK;
 }
+STO_API int sto_debug_grid_cta_block(unsigned long long *out, int count) {
+    STO_CUDA(cudaMemcpyFromSymbol(out, g_grid_cta_block, sizeof(unsigned long long) * count));
+    return STO_OK;
+}
 STO_API int sto_debug_grid_timeline(unsigned long long *out, int count) {
     STO_CUDA(cudaMemcpyFromSymbol(out, g_grid_timeline, sizeof(unsigned long long) * count));
     return STO_OK;

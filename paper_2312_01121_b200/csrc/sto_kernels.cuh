@@ -186,10 +186,16 @@ struct RowState {
 enum { kSlotM = 0, kSlotS = 1, kSlotAcc = 2, kSlotK3 = 3 };
 
 #ifdef STO_TIMELINE
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 // debug build (tools/grid_timeline.py): clock64 stamps of CTA 0 thread 0 for
 // stages [100, 116): 0 stage start, 1 x staged, 2 block phase done, 3 row phase
 // done, 4 barrier passed
 __device__ unsigned long long g_grid_timeline[16][5];
+__device__ unsigned long long g_grid_cta_block[2][1024];  // per CTA: block-phase start / end, stage 100
 #define GTL(e, ev)                                                                   \
     do {                                                                             \
         if (blockIdx.x == 0 && threadIdx.x == 0 && (e) >= 100 && (e) < 116)          \
@@ -264,6 +270,9 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
         const int stage = (int)(e & 3);
         const long long step = (e >> 2) + 1;
         GTL(e, 0);
+#ifdef STO_TIMELINE
+        if (e == 100 && threadIdx.x == 0) g_grid_cta_block[0][blockIdx.x] = globaltimer_ns();
+#endif
         // ---------------- block phase: tree nodes of W . x ----------------
         for (int ch = 0; ch < nchunks; ++ch) {
             const int x_base = ch * p.chunk_cols;
@@ -307,6 +316,9 @@ __global__ void __launch_bounds__(512, 1) grid_rk4_kernel(const __grid_constant_
             __syncthreads();
         }
         GTL(e, 2);
+#ifdef STO_TIMELINE
+        if (e == 100 && threadIdx.x == 0) g_grid_cta_block[1][blockIdx.x] = globaltimer_ns();
+#endif
         // ---------------- row phase: RHS + RK4 stage update ----------------
         const long long rec = (integrate && stage == 3)
                                   ? record_index(step, p.stride, p.steps, p.n_records)

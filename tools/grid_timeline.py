@@ -24,3 +24,13 @@ t = np.array(buf, dtype=np.float64).reshape(16, 5)
 for s in range(15):
     d = np.diff(t[s])
     print(f"stage {100+s}: x-stage {d[0]:6.0f}  block {d[1]:6.0f}  rows {d[2]:6.0f}  barrier {d[3]:6.0f}  total {t[s+1,0]-t[s,0]:6.0f} cyc")
+
+cb = (ctypes.c_ulonglong * 2048)()
+L.sto_debug_grid_cta_block(cb, 2048)
+a = np.array(cb, dtype=np.float64).reshape(2, 1024)[:, :be.plan_info["grid"]]
+start, end = a[0] - a[0].min(), a[1] - a[0].min()
+dur = a[1] - a[0]
+print(f"stage 100 block phase per CTA (globaltimer ns): start spread {start.max():.0f}, "
+      f"duration min {dur.min():.0f} median {np.median(dur):.0f} max {dur.max():.0f}, "
+      f"end spread {end.max() - end.min():.0f}")
+print("slowest CTAs:", np.argsort(-dur)[:8].tolist(), "fastest:", np.argsort(dur)[:8].tolist())
