@@ -138,3 +138,29 @@ def test_total_b_matches_reference(plugged):
     got = sto.total_b(m, u, top, sto.PhysicalParams())
     want = plugged.total_b(m, u, top_ref, plugged.PhysicalParams())
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_integration_md_ctypes_stub_runs(plugged):
+    """the ctypes stub a spinosc maintainer would paste -- executed
+    verbatim (library path substituted) and checked against spinosc's own fused backend."""
+    import re
+
+    from conftest import ROOT
+
+    text = (ROOT / "INTEGRATION.md").read_text()
+    sec = text[text.index("## 3. Bind the C ABI directly"):]
+    code = re.search(r"```python\n(.*?)```", sec, re.S).group(1)
+    lib = str(ROOT / "paper_2312_01121_b200" / "libsto_b200.so")
+    code = code.replace('ctypes.CDLL("libsto_b200.so")', f'ctypes.CDLL("{lib}")')
+    ns: dict = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    sp = plugged
+    top = sp.build_topology(150, seed=2)
+    params = sp.PhysicalParams()
+    be = ns["StoBackend"](top, params)
+    m = sp.initial_state(150)
+    states = be.integrate_run(m, np.zeros((1, 1)), 1, 1e-11, 300, 100)
+    want = sp.integrate(top, params, sp.RunConfig(n=150, steps=300, dt=1e-11, record_stride=100,
+                                                  backend="fused"), backend=None)
+    assert np.array_equal(states.view(np.uint64), want.states.view(np.uint64))
