@@ -465,7 +465,8 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
     backend._plan.last_status()
     total_s = t_start.elapsed_time(t_stop) / 1e3
-    kernel_s = float(np.mean([a.elapsed_time(b) for a, b in zip(kstart, kstop)])) / 1e3
+    per_run_ms = [a.elapsed_time(b) for a, b in zip(kstart, kstop)]
+    kernel_s = float(np.mean(per_run_ms)) / 1e3
     if dist:
         t = torch.tensor([total_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -550,7 +551,9 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": "oscillator-steps/s", "value": value, "unit": "osc-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_s * 1e3 / args.steps, "higher_is_better": True,
+            "ms_per_step": total_s * 1e3 / args.steps,
+            "ms_per_step_std": float(np.std(per_run_ms)),  # population std of the K runs (ref bench.py:196)
+            "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": ("synthetic (build_topology_device(n, seed=0): reference draws, rho from device "
                      "matvecs)" if n > 20000 else "synthetic (build_topology(n, seed=0), u=0 / "
