@@ -515,7 +515,8 @@ def run_ours(args, rank, world, local_rank):
     peaks = measured_peaks()
     alg_bytes = 32.0 * rows_mine * n * steps  # one f64 W row per RK stage per (own) osc-step
     achieved = alg_bytes / kernel_s / 1e9
-    kname = {"tiny": "tiny_rk4_kernel", "reg": "reg_rk4_kernel", "single": "grid_rk4_kernel[Shared,single]",
+    kname = {"tiny": "tiny_rk4_kernel", "reg": "reg_rk4_kernel", "cluster": "clu_rk4_kernel",
+             "single": "grid_rk4_kernel[Shared,single]",
              "resident": "grid_rk4_kernel[Shared]",
              "stream": "grid_rk4_kernel[GlobalStream]"}.get(info["kernel_name"], info["kernel_name"])
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],

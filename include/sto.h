@@ -87,6 +87,8 @@ typedef struct {
 #define STO_PLAN_NO_TINY        0x8  /* do not use the one-warp kernel for n<=32  */
 #define STO_PLAN_FORCE_REG      0x10 /* W register-resident teams (n <= 1024)     */
 #define STO_PLAN_NO_REG         0x20 /* do not use the register-resident kernel    */
+#define STO_PLAN_FORCE_CLUSTER  0x40 /* one thread-block cluster, DSMEM exchange (n <= 256) */
+#define STO_PLAN_NO_CLUSTER     0x80 /* do not use the cluster kernel              */
 
 typedef struct {
     double *m;               /* device (n,3): initial state in, final state out    */
@@ -108,7 +110,7 @@ typedef struct {
 
 typedef struct {
     int32_t kernel;          /* 0 tiny, 1 single-CTA, 2 SMEM-resident grid, 3 streaming grid,
-                                4 register-resident teams */
+                                4 register-resident teams, 5 thread-block cluster */
     int32_t grid;            /* CTAs of the persistent kernel                        */
     int32_t threads;         /* threads per CTA                                      */
     int32_t smem_bytes;      /* dynamic shared memory per CTA                        */

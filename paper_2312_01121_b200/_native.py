@@ -24,7 +24,8 @@ STO_OK, STO_E_UNAVAILABLE, STO_E_PARAM, STO_E_DIVERGED, STO_E_CUDA, STO_E_NOMEM 
 # flags of sto_plan_desc (include/sto.h)
 FORCE_STREAM, FORCE_RESIDENT, FORCE_SINGLE, NO_TINY, FORCE_REG, NO_REG = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20)
-KERNEL_NAMES = {0: "tiny", 1: "single", 2: "resident", 3: "stream", 4: "reg"}
+FORCE_CLUSTER, NO_CLUSTER = 0x40, 0x80
+KERNEL_NAMES = {0: "tiny", 1: "single", 2: "resident", 3: "stream", 4: "reg", 5: "cluster"}
 
 _c_double_p = ctypes.POINTER(ctypes.c_double)
 

@@ -14,6 +14,7 @@
 #include "../../include/sto.h"
 #include "sto_kernels.cuh"
 #include "sto_reg_kernel.cuh"
+#include "sto_cluster_kernel.cuh"
 #include "sto_ensemble_kernel.cuh"
 #include "sto_build.cuh"
 
@@ -106,6 +107,7 @@ __global__ void permute_rows_kernel(const double *__restrict__ src, long long ld
 }
 
 constexpr int kMaxFlags = 1024;
+constexpr int kClusterMaxN = 256;  // cluster kernel: W of n <= 256 fits 8 SMs' registers
 
 // logical row-major (zero padded to np x np) copy of W from the device layout
 // Ensemble W in DMMA fragment order for row tiles of TR = 8U rows
@@ -189,7 +191,7 @@ int upload_layout(Layout &L, int rows, int cols, const double *a, long long lda,
     return STO_OK;
 }
 
-enum KernelKind { kTiny = 0, kSingle = 1, kResident = 2, kStream = 3, kReg = 4 };
+enum KernelKind { kTiny = 0, kSingle = 1, kResident = 2, kStream = 3, kReg = 4, kCluster = 5 };
 
 }  // namespace
 
@@ -217,6 +219,7 @@ struct sto_plan {
     int threads = 512;
     int team = 0;  // kReg: threads per row
     int rows_per_team = 1;
+    int clu_cols = 0;  // kCluster: W columns per thread (grid = cluster size)
     // row sharding (world > 1)
     int world = 1, rank = 0;
     long long row_begin = 0;
@@ -306,6 +309,42 @@ int launch_reg_t(const RegParams &rp, int grid, int threads, size_t smem, cudaSt
 // (team T, columns per thread C, rows per team R): n <= 128 uses C = 32 in
 // one CTA; larger n uses C = 16 over the grid, R = 2 rows per team for the
 // 64-thread teams (each shared-memory x load then feeds two rows).
+template <int T, int C>
+int launch_clu_t(const KParams &p, int K, int threads, size_t smem, cudaStream_t stream) {
+    auto fn = clu_rk4_kernel<T, C>;
+    STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(K);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    STO_CUDA(cudaLaunchKernelEx(&cfg, fn, p));
+    return STO_OK;
+}
+
+// (team T, columns per thread C) of the cluster kernel; P = T*C padded row
+int launch_clu(const KParams &p, int team, int cols, int K, int threads, size_t smem, cudaStream_t s) {
+    if (cols == 32) {
+        switch (team) {
+            case 2: return launch_clu_t<2, 32>(p, K, threads, smem, s);
+            case 4: return launch_clu_t<4, 32>(p, K, threads, smem, s);
+            default: return launch_clu_t<8, 32>(p, K, threads, smem, s);
+        }
+    }
+    switch (team) {
+        case 4: return launch_clu_t<4, 16>(p, K, threads, smem, s);
+        case 8: return launch_clu_t<8, 16>(p, K, threads, smem, s);
+        default: return launch_clu_t<16, 16>(p, K, threads, smem, s);
+    }
+}
+
 int launch_reg(const RegParams &rp, int team, int rows_per_team, bool single, int grid,
                int threads, size_t smem, cudaStream_t s) {
     if (single) {
@@ -477,7 +516,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     // ---- choose the integrate kernel ------------------------------------
     const int fl = d->flags;
     const int forced = fl & (STO_PLAN_FORCE_STREAM | STO_PLAN_FORCE_RESIDENT |
-                             STO_PLAN_FORCE_SINGLE | STO_PLAN_FORCE_REG);
+                             STO_PLAN_FORCE_SINGLE | STO_PLAN_FORCE_REG | STO_PLAN_FORCE_CLUSTER);
     const size_t single_smem = grid_smem(n, cs, cs.ldw, true);
     int pw = 32;
     while (pw < n) pw <<= 1;
@@ -503,6 +542,25 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         P->kind = kTiny;
         P->grid = 1;
         P->threads = 32;
+    } else if ((fl & STO_PLAN_FORCE_CLUSTER) ||
+               (!forced && !(fl & STO_PLAN_NO_CLUSTER) && n <= kClusterMaxN)) {
+        if (n > kClusterMaxN) return bail(fail(STO_E_PARAM, "cluster kernel needs n <= 256"));
+        P->kind = kCluster;
+        const int pc = std::max(pw, 64);  // padded row P = T*C: T = 2..8 with C = 32
+        int cols = 32;
+        if (const char *e = getenv("STO_CLU_C")) cols = atoi(e) == 16 ? 16 : 32;
+        // CTA b owns the SEG = P/K rows whose x positions are [b*SEG, (b+1)*SEG):
+        // one owner warp per CTA (SEG <= 32), K a power of two (tools/clu_sweep.py)
+        int K = std::max(2, pc / 32);
+        if (const char *e = getenv("STO_CLU_K")) K = std::max(1, std::min(atoi(e), kCluMaxK));
+        P->team = pc / cols;
+        P->clu_cols = cols;
+        P->grid = K;
+        P->rows_cap = pc / K;
+        P->threads = clu_threads(P->rows_cap, P->team);
+        P->smem = clu_smem_bytes(pc);
+        if ((K & (K - 1)) || P->rows_cap > 32 || P->threads > (cols == 32 ? 288 : 576) || P->team > 32)
+            return bail(fail(STO_E_PARAM, "cluster kernel does not fit (K a power of two, P/K <= 32 rows per CTA)"));
     } else if ((fl & STO_PLAN_FORCE_REG) || (!forced && !(fl & STO_PLAN_NO_REG) && n <= 1024)) {
         if (n > 1024) return bail(fail(STO_E_PARAM, "register-resident kernel needs n <= 1024"));
         P->kind = kReg;
@@ -591,7 +649,7 @@ int sto_plan_get_info(const sto_plan *P, sto_plan_info *info) {
     if (!P || !info) return fail(STO_E_PARAM, "null plan or info");
     info->kernel = P->kind;
     info->grid = P->grid;
-    info->threads = (P->kind == kTiny || P->kind == kReg) ? P->threads : kThreads;
+    info->threads = (P->kind == kTiny || P->kind == kReg || P->kind == kCluster) ? P->threads : kThreads;
     info->smem_bytes = (int)P->smem;
     info->ldw = P->L.cs.ldw;
     info->block_cols = P->L.cs.blk;
@@ -672,6 +730,9 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
                             P->smem, s);
             break;
         }
+        case kCluster:
+            rc = launch_clu(p, P->team, P->clu_cols, P->grid, P->threads, P->smem, s);
+            break;
         case kSingle: rc = launch_grid<WSrc::Shared, true>(p, 1, P->smem, false, s); break;
         case kResident: rc = launch_grid<WSrc::Shared, false>(p, P->grid, P->smem, true, s); break;
         default:

@@ -1,0 +1,363 @@
+// sto_cluster_kernel.cuh -- small reservoirs (33 <= n <= 256): ONE thread-block
+// cluster of K CTAs (K <= 8, one per SM), W held in registers, the stage
+// x-vector pushed into every CTA's shared memory with `st.async` (DSMEM).
+//
+// The single-CTA kernel spends ~1.1 k cycles per stage on the GEMV of all n
+// rows on one SM and another ~0.5 k on the full right-hand side; splitting
+// the rows over a cluster divides the GEMV by K, and the exchange is a
+// ONE-WAY bulk copy into every peer's shared memory, no barrier round trip.
+//
+// Row ownership follows the x layout.  The GEMV reads x "team-blocked"
+// (position of column col = ((q>>1)*T + j)*2 + (q&1), j = col / C, q = col % C:
+// team lane j's 16-byte loads are consecutive words, no bank conflicts).  CTA
+// b owns the rows whose x POSITIONS are the segment [b*SEG, (b+1)*SEG),
+// SEG = P/K, so the x values it publishes each stage are one contiguous,
+// 16-byte aligned run of SEG doubles (pad positions, columns >= n, stay +0.0):
+//
+//   owner warp of CTA b                               every CTA c of the cluster
+//   -------------------                               --------------------------
+//   x of its SEG rows -> staging[buf] (STS),
+//   fence.proxy.async, __syncwarp, lane c:
+//   cp.async.bulk shared::cta -> shared::cluster ---->  xs[buf][b*SEG ...], complete_tx
+//                                                        on mbarrier[buf] of CTA c
+//
+// (8-byte `st.async` per row and destination cost ~100 cycles per warp-wide
+// store -- 0.4-0.6 k cycles of every stage at K = 4 -- one bulk copy per
+// destination replaces K*SEG remote stores by K requests.)  Each CTA arms
+// mbarrier[buf] with expect_tx(8 P) for the next stage right after waiting on
+// the current one (the remote bytes of a phase cannot arrive before the CTA
+// has completed the previous phase of that buffer: a peer can only publish
+// stage e+1 after it received this CTA's stage-e values, which are published
+// after this CTA's stage e-1 GEMV -- so two buffers suffice and no cluster
+// barrier is needed on the hot path).  Stage e reads buffer e & 1 = stage & 1
+// (four stages per step), so the buffer index and the mbarrier parity are
+// compile-time constants of the unrolled stage loop.
+//
+// Warp roles: GEMV teams (T threads per row, C = 16/32 W columns per thread in
+// registers, row padded to P = T*C with W = -0.0 / x = +0.0; in-register
+// pinned tree + xor butterfly = the reference's padded aligned tree,
+// bit-exact) hand the row sums to ONE owner warp (RK state in registers) via
+// shared memory and a named barrier; the owner warp's own-state RHS half
+// (row_rhs_pre, with the IEEE division) runs while the GEMV warps wait for the
+// exchange and compute the next GEMV.
+//
+// Divergence: on recording steps the owners check their state and every CTA
+// meets at one `barrier.cluster`, then reads all K "bad" flags through DSMEM,
+// so all CTAs stop after the same step (integrator.py:174-177).
+#pragma once
+
+#include "sto_reg_kernel.cuh"
+
+namespace sto {
+
+constexpr int kCluMaxK = 8;
+
+__device__ __forceinline__ uint32_t clu_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t clu_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t clu_size() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t clu_mapa(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// 8-byte remote store into CTA-cluster shared memory, completion counted on
+// the destination CTA's mbarrier (both given as cluster addresses)
+__device__ __forceinline__ void clu_st_async(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void clu_bar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void clu_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void clu_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "CLU_WAIT_%=:\n\t"
+#ifdef STO_CLU_WAIT_CTA
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+#else
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+#endif
+        "@!p bra CLU_WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void clu_sync() {  // every thread of every CTA of the cluster
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+__device__ __forceinline__ int clu_ld_s32(uint32_t raddr) {
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(raddr) : "memory");
+    return v;
+}
+
+#ifdef STO_TIMELINE
+// the stamp takes `after` as an operand, so it cannot be scheduled before the
+// value it is meant to follow is computed
+__device__ __forceinline__ void clu_tl(long long e, int ev, bool me, double after) {
+    const int who = blockIdx.x == 0 ? 0 : (blockIdx.x == gridDim.x - 1 ? 1 : -1);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) : "d"(after) : "memory");
+    if (me && who >= 0 && e >= kTlFirst && e < kTlFirst + kTlStages) g_timeline[who][e - kTlFirst][ev] = t;
+}
+#define CTL(e, ev, me, after) clu_tl((e), (ev), (me), (after))
+#else
+#define CTL(e, ev, me, after)
+#endif
+
+// shared-memory bytes of the cluster kernel for a padded row of P columns
+// (x double buffer, row sums, staging double buffer, mbarriers, flag)
+__host__ __device__ constexpr size_t clu_smem_bytes(int P) {
+    return sizeof(double) * (2 * (size_t)P + 32 + 2 * 32) + 2 * sizeof(unsigned long long) + 16;
+}
+// threads of one CTA: one owner warp (SEG <= 32 rows) + the GEMV teams
+__host__ __device__ constexpr int clu_threads(int seg, int team) {
+    return 32 + 32 * ((seg * team + 31) / 32);
+}
+// column (= oscillator) whose x sits at team-blocked position `pos`
+// (inverse of reg_xpos<C>)
+__device__ __forceinline__ int clu_col_at(int pos, int T, int C) {
+    const int e = pos & 1, jj = (pos >> 1) % T, a = (pos >> 1) / T;
+    return jj * C + 2 * a + e;
+}
+
+// 32 W columns per thread need > 128 registers: those variants run <= 288 threads
+template <int T, int C>
+__global__ void __launch_bounds__(C == 32 ? 288 : 576, 1) clu_rk4_kernel(const __grid_constant__ KParams p) {
+    constexpr int P = T * C;
+    constexpr int LV = (C == 32) ? 5 : 4;  // tree levels above the products
+    static_assert(T <= 32, "team butterfly stays inside one warp");
+    extern __shared__ __align__(16) double smem[];
+    double *xs = smem;        // [2][P] team-blocked x, double-buffered by stage parity
+    double *cps = xs + 2 * P;  // [32] row sums, GEMV teams -> owners
+    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(cps + 32 + 2 * 32);
+    volatile int *sbad = reinterpret_cast<volatile int *>(mbar + 2);
+    volatile long long *zslot = reinterpret_cast<volatile long long *>(mbar + 3);  // always 0
+
+    const int K = (int)clu_size(), b = (int)clu_rank();
+    const int n = p.rows;
+    const int SEG = P / K;  // x positions (rows) owned by this CTA: [b*SEG, (b+1)*SEG)
+    const int g0 = 32;      // threads [0, 32): owner warp; [32, ...): GEMV teams
+    const bool gemv_warp = (int)threadIdx.x >= g0;
+    // GEMV role: team `row`, member j -- columns [C*j, C*j + C) of row kg
+    const int t = (int)threadIdx.x - g0;
+    const int row = gemv_warp ? t / T : 0, j = gemv_warp ? t % T : 0;
+    const int kg = (gemv_warp && row < SEG) ? clu_col_at(b * SEG + row, T, C) : n;
+    // RHS role: lane r of the owner warp owns oscillator k (RK state in registers)
+    const int r = threadIdx.x;
+    const int k = (!gemv_warp && r < SEG) ? clu_col_at(b * SEG + r, T, C) : n;
+    const bool owner = k < n;
+
+    double w[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        const int col = j * C + q;
+        w[q] = (kg < n && col < n) ? p.w[(size_t)kg * p.cs.ldw + col_perm(p.cs, col)] : -0.0;
+    }
+    for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) xs[i] = 0.0;
+    __syncthreads();
+    for (int col = threadIdx.x; col < n; col += blockDim.x) xs[reg_xpos<C>(col, T)] = p.m[3 * (size_t)col];
+    const uint32_t bar0 = clu_u32(mbar), bar1 = clu_u32(mbar + 1);
+    if (threadIdx.x == 0) {
+        clu_bar_init(bar0, 1);
+        clu_bar_init(bar1, 1);
+        *sbad = 0;
+        *zslot = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    V3 m{0.0, 0.0, 0.0}, s{0.0, 0.0, 0.0}, acc{0.0, 0.0, 0.0}, k3{0.0, 0.0, 0.0};
+    if (owner) {
+        m = V3{p.m[3 * (size_t)k], p.m[3 * (size_t)k + 1], p.m[3 * (size_t)k + 2]};
+        if (p.states) {
+            double *st = p.states + 3 * (size_t)k;
+            st[0] = m.x;
+            st[1] = m.y;
+            st[2] = m.z;
+        }
+    }
+    clu_sync();  // every CTA's mbarriers and buffers are initialised before any st.async
+    const uint32_t xbytes = 8u * (uint32_t)n;  // one 8-byte store per oscillator
+    const unsigned nthreads = blockDim.x;
+    bool stop = false;
+
+    if (gemv_warp) {
+        // ==================== GEMV teams ====================================
+        if (t == 0) clu_expect(bar1, xbytes);  // x of stage 1
+        long long next_rec = p.stride;
+        for (long long step = 1; step <= p.steps && !stop; ++step) {
+            const bool record = (step == next_rec) || (step == p.steps);
+#pragma unroll
+            for (int stage = 0; stage < 4; ++stage) {
+                const long long estage = (step - 1) * 4 + stage;
+                const int buf = stage & 1;  // compile-time after unrolling
+                if (!(step == 1 && stage == 0)) {
+                    // phases of buffer 1: stages 1, 3 -> parity 0, 1; buffer 0: stages 2, 0 -> 0, 1
+                    clu_wait(buf ? bar1 : bar0, (stage == 1 || stage == 2) ? 0u : 1u);
+                    if (t == 0) clu_expect(buf ? bar0 : bar1, xbytes);  // the next stage's buffer
+                }
+                CTL(estage, 3, t == 0, 0.0);
+                const double *xb = xs + buf * P;
+                double lvl[LV];
+#pragma unroll
+                for (int i = 0; i < C / 2; ++i) {
+                    const double2 x2 = *reinterpret_cast<const double2 *>(xb + ((i * T + j) << 1));
+                    double node = radd(rmul(w[2 * i], x2.x), rmul(w[2 * i + 1], x2.y));
+#pragma unroll
+                    for (int l = 0; l < LV - 1; ++l) {
+                        if (i & (1 << l)) node = radd(lvl[l], node);
+                        else { lvl[l] = node; break; }
+                    }
+                    if (i == C / 2 - 1) lvl[LV - 1] = node;
+                }
+                double cp = lvl[LV - 1];
+#pragma unroll
+                for (int mask = 1; mask < T; mask <<= 1) cp = radd(cp, __shfl_xor_sync(0xffffffffu, cp, mask));
+                if (j == 0 && row < SEG) cps[row] = cp;
+                CTL(estage, 4, t == 0, cp);
+                asm volatile("bar.arrive 1, %0;" ::"r"(nthreads) : "memory");
+                if (stage == 3 && record) {  // cluster-wide stop decision (uniform branch)
+                    clu_sync();
+                    const uint32_t fl = clu_u32((const void *)sbad);
+                    for (int c = 0; c < K; ++c) stop |= clu_ld_s32(clu_mapa(fl, c)) != 0;
+                    if (stop) break;
+                }
+            }
+            if (record && step == next_rec) next_rec += p.stride;
+        }
+    } else {
+        // ==================== owners: RHS, RK4 update, publication ==========
+        const int lane = threadIdx.x;
+        auto u_of = [&](long long st) {  // drive sample of step `st` (zero-order hold, model.py:93-149)
+            return p.n_samples > 1 ? p.samples + ((st - 1) / p.sps) * p.n_in : p.samples;
+        };
+        const double win = (owner && p.n_in == 1) ? p.w_in[k] : 0.0;
+        auto cin_of = [&](long long st) {
+            return (p.n_in == 1) ? rmul(win, u_of(st)[0]) : tree_dot_stream(p.w_in + (size_t)k * p.n_in, u_of(st), p.n_in);
+        };
+        double cin = 0.0, u_next = 0.0;
+        RhsPre pre{};
+        if (owner) {
+            cin = cin_of(1);
+            pre = row_rhs_pre(m, cin, p.c);
+        }
+        long long next_rec = p.stride;
+        long long rec_idx = 1;
+        for (long long step = 1; step <= p.steps && !stop; ++step) {
+            const bool record = (step == next_rec) || (step == p.steps);
+#pragma unroll
+            for (int stage = 0; stage < 4; ++stage) {
+                const long long estage = (step - 1) * 4 + stage;
+                // row sums in cps.  `pre` is tied to the barrier so the compiler cannot
+                // sink the own-state half (IEEE division included) past it: it must
+                // run while the GEMV warps work, not after the row sums arrive
+                asm volatile("bar.sync 1, %8;"
+                             : "+d"(pre.m.x), "+d"(pre.m.y), "+d"(pre.m.z), "+d"(pre.hs_qx), "+d"(pre.by),
+                               "+d"(pre.bz), "+d"(pre.ax), "+d"(pre.ain_cin)
+                             : "r"(nthreads)
+                             : "memory");
+                CTL(estage, 0, threadIdx.x == 0, 0.0);
+                double xpub = 0.0;
+                bool bad = false;
+                if (owner) {
+                    const V3 d = row_rhs_post(pre, cps[r], p.c);
+                    if (stage == 0) {
+                        acc = d;
+                        s = stage_point(m, d, p.h2);
+                        xpub = s.x;
+                    } else if (stage == 1) {
+                        acc = acc_k2(acc, d);
+                        s = stage_point(m, d, p.h2);
+                        xpub = s.x;
+                    } else if (stage == 2) {
+                        k3 = d;
+                        s = stage_point(m, d, p.dt);
+                        xpub = s.x;
+                    } else {
+                        m = rk4_final(m, acc, k3, d, p.dt6);
+                        xpub = m.x;
+                        if (record) {
+                            if (!all_finite(m)) {
+                                bad = true;
+                                report_divergence(p.status, step, k);
+                            } else if (p.states) {
+                                const long long ri = (step == next_rec) ? rec_idx : p.n_records - 1;
+                                double *st = p.states + ((size_t)ri * n + k) * 3;
+                                st[0] = m.x;
+                                st[1] = m.y;
+                                st[2] = m.z;
+                            }
+                        }
+                    }
+                }
+                CTL(estage, 1, threadIdx.x == 0, xpub);
+                if (stage == 3 && record) {
+                    if (bad) *sbad = 1;
+                    clu_sync();
+                    const uint32_t fl = clu_u32((const void *)sbad);
+                    for (int c = 0; c < K; ++c) stop |= clu_ld_s32(clu_mapa(fl, c)) != 0;
+                    if (stop) break;
+                }
+                const bool last = (step == p.steps) && stage == 3;
+                if (owner && !last) {
+                    // publication: one 8-byte st.async per destination CTA (the cheapest
+                    // of the variants measured, tools/clu_sweep.py / DESIGN.md)
+                    const int nb = (stage + 1) & 1;  // destination buffer (compile-time)
+                    const uint32_t xa = clu_u32(xs + nb * P + b * SEG + r);
+#pragma unroll
+                    for (int c = 0; c < kCluMaxK; ++c)
+                        if (c < K) clu_st_async(clu_mapa(xa, c), xpub, clu_mapa(nb ? bar1 : bar0, c));
+                }
+                // keep the next stage's own-state half (which reads s / m) after the
+                // stores: ptxas hoists that independent arithmetic (its IEEE division
+                // included) above the remote stores, onto the critical path.  OR-ing the
+                // inputs' bits with a zero loaded from shared memory AFTER the stores
+                // makes them depend on that load (bits unchanged)
+                if (!last) {
+                    const long long z = *zslot;
+                    auto pin = [z](double v) { return __longlong_as_double(__double_as_longlong(v) | z); };
+                    if (stage < 3) s = V3{pin(s.x), pin(s.y), pin(s.z)};
+                    else m = V3{pin(m.x), pin(m.y), pin(m.z)};
+                }
+                CTL(estage, 2, threadIdx.x == 0, 0.0);
+                if (owner && !last) {
+                    // own-state half of the next stage's RHS, while the other
+                    // warps wait for the exchange and run the next GEMV
+                    if (stage == 0 && p.n_in == 1 && step < p.steps) u_next = u_of(step + 1)[0];  // prefetch
+                    if (stage < 3) {
+                        pre = row_rhs_pre(s, cin, p.c);
+                    } else {
+                        cin = p.n_in == 1 ? rmul(win, u_next) : cin_of(step + 1);
+                        pre = row_rhs_pre(m, cin, p.c);
+                    }
+                }
+            }
+            if (record && step == next_rec) {
+                next_rec += p.stride;
+                ++rec_idx;
+            }
+        }
+        if (owner) {
+            double *mm = p.m + 3 * (size_t)k;
+            mm[0] = m.x;
+            mm[1] = m.y;
+            mm[2] = m.z;
+        }
+    }
+    clu_sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
+}  // namespace sto

@@ -227,7 +227,9 @@ __global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __
             if constexpr (SINGLE) {
                 if (owner) xs[reg_xpos<C>(k, T)] = xpub;
                 if (bad) *sstop = 1;
+                TL(estage, 2);
                 __syncthreads();
+                TL(estage, 3);
                 if (*sstop) stop = true;
             } else {
                 ++epoch;

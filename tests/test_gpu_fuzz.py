@@ -22,7 +22,7 @@ from conftest import assert_bit_equal
 pytestmark = pytest.mark.gpu
 
 FORCE = {"auto": 0, "tiny": 0, "single": 0x4 | 0x8, "resident": 0x2 | 0x8, "stream": 0x1 | 0x8,
-         "reg": 0x10 | 0x8}
+         "reg": 0x10 | 0x8, "cluster": 0x40 | 0x8}
 
 
 @st.composite
@@ -46,6 +46,8 @@ def _families(n):
     fams = ["auto", "stream", "resident"]
     if n <= 1024:
         fams.append("reg")
+    if n <= 256:
+        fams.append("cluster")
     if n <= 32:
         fams.append("tiny")
     if n <= 128:

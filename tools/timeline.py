@@ -3,7 +3,8 @@ import ctypes, sys
 import numpy as np
 sys.path.insert(0, ".")
 import paper_2312_01121_b200._native as nat
-nat.LIB_PATH = nat.LIB_PATH.with_name("libsto_b200_timeline.so")
+import os
+nat.LIB_PATH = nat.LIB_PATH.with_name(os.environ.get("STO_LIB", "libsto_b200_timeline.so"))
 import paper_2312_01121_b200 as sto
 from paper_2312_01121_b200.backends.b200 import B200Backend
 
@@ -26,4 +27,11 @@ for who in range(2):
     for s in range(16):
         row = t[who, s] - t0
         d = np.diff(t[who, s])
+        if be.plan_info["kernel_name"] == "cluster":
+            # events: 0 owner has row sums, 1 post+update done, 2 published,
+            #         3 GEMV warp got x, 4 GEMV butterfly done
+            nx = t[who, s + 1] if s < 15 else t[who, s] * np.nan
+            print(f"  stage {400+s}: cycle {nx[0] - t[who, s, 0]:6.0f}  post {d[0]:5.0f}  publish {d[1]:5.0f}  "
+                  f"exchange {nx[3] - t[who, s, 2]:6.0f}  gemv {nx[4] - nx[3]:5.0f}  handoff {nx[0] - nx[4]:5.0f}")
+            continue
         print(f"  stage {400+s}: start {row[0]:8.0f} cyc gemv {d[0]:6.0f}  rhs {d[1]:6.0f}  ll {d[2]:6.0f}  sync {d[3]:6.0f}  total->{(t[who, s+1, 0] - t[who, s, 0]) if s < 15 else 0:6.0f}")
