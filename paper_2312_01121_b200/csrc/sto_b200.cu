@@ -547,11 +547,13 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         if (n > kClusterMaxN) return bail(fail(STO_E_PARAM, "cluster kernel needs n <= 256"));
         P->kind = kCluster;
         const int pc = std::max(pw, 64);  // padded row P = T*C: T = 2..8 with C = 32
-        int cols = 32;
-        if (const char *e = getenv("STO_CLU_C")) cols = atoi(e) == 16 ? 16 : 32;
         // CTA b owns the SEG = P/K rows whose x positions are [b*SEG, (b+1)*SEG):
-        // one owner warp per CTA (SEG <= 32), K a power of two (tools/clu_sweep.py)
-        int K = std::max(2, pc / 32);
+        // one owner warp per CTA (SEG <= 32), K a power of two.  Fastest measured
+        // (tools/clu_sweep.py): P = 64 -> K = 2, C = 32; P = 128 -> K = 8, C = 16;
+        // P = 256 -> K = 8, C = 32
+        int cols = pc == 128 ? 16 : 32;
+        if (const char *e = getenv("STO_CLU_C")) cols = atoi(e) == 16 ? 16 : 32;
+        int K = pc == 64 ? 2 : 8;
         if (const char *e = getenv("STO_CLU_K")) K = std::max(1, std::min(atoi(e), kCluMaxK));
         P->team = pc / cols;
         P->clu_cols = cols;

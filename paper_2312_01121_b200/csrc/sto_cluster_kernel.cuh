@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(C == 32 ? 288 : 576, 1) clu_rk4_kernel(const _
     extern __shared__ __align__(16) double smem[];
     double *xs = smem;        // [2][P] team-blocked x, double-buffered by stage parity
     double *cps = xs + 2 * P;  // [32] row sums, GEMV teams -> owners
+    double *stg = cps + 32;    // [32] this CTA's published x, owners -> fan-out warps
     unsigned long long *mbar = reinterpret_cast<unsigned long long *>(cps + 32 + 2 * 32);
     volatile int *sbad = reinterpret_cast<volatile int *>(mbar + 2);
     volatile long long *zslot = reinterpret_cast<volatile long long *>(mbar + 3);  // always 0
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(C == 32 ? 288 : 576, 1) clu_rk4_kernel(const _
     const int t = (int)threadIdx.x - g0;
     const int row = gemv_warp ? t / T : 0, j = gemv_warp ? t % T : 0;
     const int kg = (gemv_warp && row < SEG) ? clu_col_at(b * SEG + row, T, C) : n;
+    const int kpub = (gemv_warp && (t & 31) < SEG) ? clu_col_at(b * SEG + (t & 31), T, C) : n;  // fan-out lane's row
     // RHS role: lane r of the owner warp owns oscillator k (RK state in registers)
     const int r = threadIdx.x;
     const int k = (!gemv_warp && r < SEG) ? clu_col_at(b * SEG + r, T, C) : n;
@@ -235,6 +237,19 @@ __global__ void __launch_bounds__(C == 32 ? 288 : 576, 1) clu_rk4_kernel(const _
                     for (int c = 0; c < K; ++c) stop |= clu_ld_s32(clu_mapa(fl, c)) != 0;
                     if (stop) break;
                 }
+                if (!((step == p.steps) && stage == 3)) {
+                    // publication fan-out: the owner warp staged this CTA's x in stg; GEMV
+                    // warp gw sends it to CTAs gw, gw + nGW, ... (one 8-byte st.async per
+                    // oscillator and destination, the warps in parallel)
+                    asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+                    const int nb = (stage + 1) & 1;
+                    const int gw = t >> 5, gl = t & 31, ngw = (int)(nthreads >> 5) - 1;
+                    if (gl < SEG && kpub < n) {
+                        const double v = stg[gl];
+                        const uint32_t xa = clu_u32(xs + nb * P + b * SEG + gl);
+                        for (int c = gw; c < K; c += ngw) clu_st_async(clu_mapa(xa, c), v, clu_mapa(nb ? bar1 : bar0, c));
+                    }
+                }
             }
             if (record && step == next_rec) next_rec += p.stride;
         }
@@ -312,14 +327,9 @@ __global__ void __launch_bounds__(C == 32 ? 288 : 576, 1) clu_rk4_kernel(const _
                     if (stop) break;
                 }
                 const bool last = (step == p.steps) && stage == 3;
-                if (owner && !last) {
-                    // publication: one 8-byte st.async per destination CTA (the cheapest
-                    // of the variants measured, tools/clu_sweep.py / DESIGN.md)
-                    const int nb = (stage + 1) & 1;  // destination buffer (compile-time)
-                    const uint32_t xa = clu_u32(xs + nb * P + b * SEG + r);
-#pragma unroll
-                    for (int c = 0; c < kCluMaxK; ++c)
-                        if (c < K) clu_st_async(clu_mapa(xa, c), xpub, clu_mapa(nb ? bar1 : bar0, c));
+                if (!last) {  // hand x to the GEMV warps, which send it (fan-out above)
+                    if (owner) stg[r] = xpub;
+                    asm volatile("bar.arrive 2, %0;" ::"r"(nthreads) : "memory");
                 }
                 // keep the next stage's own-state half (which reads s / m) after the
                 // stores: ptxas hoists that independent arithmetic (its IEEE division
