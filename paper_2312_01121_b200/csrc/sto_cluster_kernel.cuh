@@ -4,42 +4,43 @@
 //
 // The single-CTA kernel spends ~1.1 k cycles per stage on the GEMV of all n
 // rows on one SM and another ~0.5 k on the full right-hand side; splitting
-// the rows over a cluster divides the GEMV by K, and the exchange is a
-// ONE-WAY bulk copy into every peer's shared memory, no barrier round trip.
+// the rows over a cluster divides the GEMV by K, and the exchange is ONE-WAY
+// remote stores into every peer's shared memory, no barrier round trip.
 //
 // Row ownership follows the x layout.  The GEMV reads x "team-blocked"
 // (position of column col = ((q>>1)*T + j)*2 + (q&1), j = col / C, q = col % C:
 // team lane j's 16-byte loads are consecutive words, no bank conflicts).  CTA
 // b owns the rows whose x POSITIONS are the segment [b*SEG, (b+1)*SEG),
-// SEG = P/K, so the x values it publishes each stage are one contiguous,
-// 16-byte aligned run of SEG doubles (pad positions, columns >= n, stay +0.0):
+// SEG = P/K <= 32 (pad positions, columns >= n, have no row and stay +0.0),
+// so every CTA has the same small number of rows and one owner warp.
 //
-//   owner warp of CTA b                               every CTA c of the cluster
-//   -------------------                               --------------------------
-//   x of its SEG rows -> staging[buf] (STS),
-//   fence.proxy.async, __syncwarp, lane c:
-//   cp.async.bulk shared::cta -> shared::cluster ---->  xs[buf][b*SEG ...], complete_tx
-//                                                        on mbarrier[buf] of CTA c
+// Per stage (e = 4*(step-1) + stage):
+//   GEMV warps   wait mbarrier[e&1] -> x_e complete in xs[e&1]
+//                pinned tree + butterfly -> row sums -> cps, bar.arrive(1)
+//   owner warp   bar.sync(1) -> cp-dependent RHS half, RK4 update -> x_{e+1}
+//                -> stg, bar.arrive(2); then the own-state half of the next
+//                stage's RHS (row_rhs_pre, IEEE division) while the others work
+//   GEMV warps   bar.sync(2) -> warp gw sends stg to CTAs gw, gw + nGW, ...:
+//                one 8-byte `st.async` per (oscillator, destination) into
+//                xs[(e+1)&1] of that CTA, complete_tx on its mbarrier[(e+1)&1]
 //
-// (8-byte `st.async` per row and destination cost ~100 cycles per warp-wide
-// store -- 0.4-0.6 k cycles of every stage at K = 4 -- one bulk copy per
-// destination replaces K*SEG remote stores by K requests.)  Each CTA arms
-// mbarrier[buf] with expect_tx(8 P) for the next stage right after waiting on
-// the current one (the remote bytes of a phase cannot arrive before the CTA
-// has completed the previous phase of that buffer: a peer can only publish
-// stage e+1 after it received this CTA's stage-e values, which are published
-// after this CTA's stage e-1 GEMV -- so two buffers suffice and no cluster
-// barrier is needed on the hot path).  Stage e reads buffer e & 1 = stage & 1
-// (four stages per step), so the buffer index and the mbarrier parity are
-// compile-time constants of the unrolled stage loop.
+// Each CTA arms mbarrier[buf] with expect_tx(8 n) for the next stage right
+// after waiting on the current one (the remote bytes of a phase cannot arrive
+// before the CTA has completed the previous phase of that buffer: a peer can
+// only publish stage e+1 after it received this CTA's stage-e values, which
+// are published after this CTA's stage e-1 GEMV -- so two buffers suffice
+// and no cluster barrier is needed on the hot path).  Stage e reads buffer
+// e & 1 = stage & 1 (four stages per step), so the buffer index and the
+// mbarrier parity are compile-time constants of the unrolled stage loop.
 //
-// Warp roles: GEMV teams (T threads per row, C = 16/32 W columns per thread in
-// registers, row padded to P = T*C with W = -0.0 / x = +0.0; in-register
-// pinned tree + xor butterfly = the reference's padded aligned tree,
-// bit-exact) hand the row sums to ONE owner warp (RK state in registers) via
-// shared memory and a named barrier; the owner warp's own-state RHS half
-// (row_rhs_pre, with the IEEE division) runs while the GEMV warps wait for the
-// exchange and compute the next GEMV.
+// Measured alternatives: the owner warp issuing all K stores
+// itself (+10 %), 16-byte paired stores (+50 %), and one cp.async.bulk of the
+// staged segment per destination (+10 %) were all slower than the fan-out.
+//
+// Team layout (as in sto_reg_kernel.cuh): T threads per row, C = 16/32 W
+// columns per thread in registers, row padded to P = T*C with W = -0.0 /
+// x = +0.0: in-register pinned tree + xor butterfly = the reference's padded
+// aligned tree, bit-exact.
 //
 // Divergence: on recording steps the owners check their state and every CTA
 // meets at one `barrier.cluster`, then reads all K "bad" flags through DSMEM,
@@ -120,7 +121,7 @@ __device__ __forceinline__ void clu_tl(long long e, int ev, bool me, double afte
 #endif
 
 // shared-memory bytes of the cluster kernel for a padded row of P columns
-// (x double buffer, row sums, staging double buffer, mbarriers, flag)
+// (x double buffer, row sums, staging, mbarriers, flags)
 __host__ __device__ constexpr size_t clu_smem_bytes(int P) {
     return sizeof(double) * (2 * (size_t)P + 32 + 2 * 32) + 2 * sizeof(unsigned long long) + 16;
 }
