@@ -29,6 +29,18 @@ int fail(int code, const std::string &msg) {
     return code;
 }
 
+// Peer watchdog of the sharded exchange (sto_kernels.cuh::multi_sync): the
+// longest a rank waits for one peer's epoch flag before it stops the run and
+// reports the peer lost.  STO_PEER_TIMEOUT_S overrides the 120 s default.
+unsigned long long peer_timeout_ns() {
+    double sec = 120.0;
+    if (const char *v = std::getenv("STO_PEER_TIMEOUT_S")) {
+        const double t = std::atof(v);
+        if (t > 0) sec = t;
+    }
+    return (unsigned long long)(sec * 1e9);
+}
+
 #define STO_CUDA(call)                                                                       \
     do {                                                                                     \
         cudaError_t _e = (call);                                                             \
@@ -231,6 +243,7 @@ struct sto_plan {
     void *ipc_opened[kMaxRanks] = {};
     bool connected = false;
     unsigned long long epoch_base = 0;  // monotonic epochs across launches
+    bool peer_lost = false;             // a run hit the peer watchdog: epochs out of step
     // ensemble resources (allocated on first sto_integrate_ensemble)
     double *ens_w = nullptr;           // np x np row-major, zero padded
     int ens_np = 0;
@@ -706,7 +719,9 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
     int rc = STO_OK;
     if (P->world > 1) {
         if (!P->connected) return fail(STO_E_PARAM, "sharded plan is not connected to its peers");
+        if (P->peer_lost) return fail(STO_E_CUDA, "sharded plan lost a peer in an earlier run; destroy it");
         p.mp.world = P->world;
+        p.mp.timeout_ns = peer_timeout_ns();
         p.mp.rank_base = P->rank;
         p.mp.ctas_per_rank = P->grid;
         p.mp.epoch_base = P->epoch_base;
@@ -974,6 +989,7 @@ int sto_integrate_group(sto_plan **plans, int32_t world, const sto_run *r, sto_s
     p.mp.rank_base = 0;
     p.mp.ctas_per_rank = per;
     p.mp.epoch_base = P0->epoch_base;
+    p.mp.timeout_ns = peer_timeout_ns();
     for (int q = 0; q < world; ++q) {
         p.mp.sh[q] = shard_info(plans[q]);
         p.mp.xbuf_of[q] = plans[q]->exch;
@@ -998,6 +1014,16 @@ int sto_plan_last_status(sto_plan *P, sto_status *status, void *stream) {
     STO_CUDA(cudaMemcpyAsync(&h, P->status, sizeof(h), cudaMemcpyDeviceToHost,
                              (cudaStream_t)stream));
     STO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    if (h.flag == 2) {
+        P->peer_lost = true;
+        status->diverged = 0;
+        status->reserved = 0;
+        status->oscillator = -1;
+        status->step = -1;
+        return fail(STO_E_CUDA, "rank " + std::to_string(h.key) +
+                                    " did not reach the x exchange within the peer watchdog limit "
+                                    "(STO_PEER_TIMEOUT_S); the run stopped early and the plan is unusable");
+    }
     status->diverged = h.flag;
     status->reserved = 0;
     status->oscillator = h.flag ? (h.key & 0xffffff) : -1;

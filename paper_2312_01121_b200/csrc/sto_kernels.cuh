@@ -34,6 +34,19 @@ __device__ __forceinline__ void report_divergence(StatusDev *st, long long step,
     st->flag = 1;
 }
 
+// status flag 2: a peer rank did not raise its epoch flag within the
+// watchdog limit (key = that rank); the run stopped early and the plan's
+// epochs are no longer in step with its peers
+__device__ __forceinline__ void report_peer_timeout(StatusDev *st, int peer) {
+    st->key = peer;
+    atomicExch(&st->flag, 2);
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 enum KernelMode : int { kIntegrate = 0, kDerivative = 1, kMatvec = 2 };
 
 // ----------------------------------------------------------------------------
@@ -67,6 +80,7 @@ struct MultiParams {
     int ctas_per_rank;
     int pad;
     unsigned long long epoch_base;  // monotonic across launches
+    unsigned long long timeout_ns;  // peer watchdog: longest wait for one epoch flag
     ShardInfo sh[kMaxRanks];        // ranks hosted by this launch
     double *xbuf_of[kMaxRanks];     // every rank's receive buffer (peer pointers)
     unsigned long long *flags_of[kMaxRanks];
@@ -143,13 +157,25 @@ __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInf
         }
     }
     if (threadIdx.x < mp.world) {
-        unsigned long long f;
-        do {
+        unsigned long long f, t0 = 0;
+        for (unsigned it = 0;; ++it) {
             asm volatile("ld.relaxed.sys.global.u64 %0, [%1];"
                          : "=l"(f)
                          : "l"(sh.flags + (size_t)threadIdx.x * kFlagSlot)
                          : "memory");
-        } while ((f & ~(1ull << 63)) < epoch);
+            if ((f & ~(1ull << 63)) >= epoch) break;
+            // watchdog: a peer that never arrives (its process died or never
+            // launched) must not hang this GPU -- report it and stop
+            if ((it & 1023u) == 1023u) {
+                const unsigned long long t = globaltimer_ns();
+                if (t0 == 0) t0 = t;
+                else if (t - t0 > mp.timeout_ns) {
+                    report_peer_timeout(const_cast<StatusDev *>(status), threadIdx.x);
+                    f = 1ull << 63;
+                    break;
+                }
+            }
+        }
         asm volatile("fence.acq_rel.sys;" ::: "memory");
         if (f >> 63) *sflag = 1;
     }
@@ -186,11 +212,6 @@ struct RowState {
 enum { kSlotM = 0, kSlotS = 1, kSlotAcc = 2, kSlotK3 = 3 };
 
 #ifdef STO_TIMELINE
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 // debug build (tools/grid_timeline.py): clock64 stamps of CTA 0 thread 0 for
 // stages [100, 116): 0 stage start, 1 x staged, 2 block phase done, 3 row phase
 // done, 4 barrier passed

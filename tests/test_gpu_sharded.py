@@ -160,3 +160,36 @@ def test_random_logical_rank_runs_bit_exact(oracle_mod, n, world, steps, sps, fa
     except sto.ParameterError:
         return  # family does not fit this shard (e.g. SMEM-resident rows too wide)
     assert_bit_equal(got, want, f"n={n} world={world} fam={fam}")
+
+
+def test_lost_peer_watchdog(monkeypatch):
+    """A rank whose peer never launches must not hang its GPU: the exchange
+    watchdog (STO_PEER_TIMEOUT_S) stops the persistent kernel and the run
+    raises SpinoscError; the plan then refuses further runs (its epochs are out
+    of step with the peer's)."""
+    import time
+
+    import torch
+
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200 import _native
+    from paper_2312_01121_b200.sharding import _shard_plan, shard_rows
+
+    monkeypatch.setenv("STO_PEER_TIMEOUT_S", "1")
+    n, world = 600, 2
+    top = sto.build_topology(n, seed=5)
+    consts = sto.kernel_scalars(sto.PhysicalParams())
+    plans = [_shard_plan(top, consts, b, c, world, r, 0) for r, (b, c) in enumerate(shard_rows(n, world))]
+    _native.connect_local(plans)
+    m = torch.as_tensor(sto.initial_state(n), device="cuda")
+    drive = torch.zeros((1, 1), dtype=torch.float64, device="cuda")
+    st = torch.empty((2, n, 3), dtype=torch.float64, device="cuda")
+    t0 = time.time()
+    with pytest.raises(sto.SpinoscError, match="did not reach"):
+        plans[0].integrate_dev(m, drive, 1, 1e-11, 20, 20, st)  # rank 1 never runs
+    assert time.time() - t0 < 30
+    with pytest.raises(sto.SpinoscError, match="lost a peer"):
+        plans[0].integrate_dev(m, drive, 1, 1e-11, 20, 20, st)
+    torch.cuda.synchronize()  # the device is still healthy
+    for p in plans:
+        p.close()
