@@ -56,13 +56,31 @@ static consts_t unpack(const double *c) {
     return k;
 }
 
-/* dm/dt of oscillator k into out[3k..3k+2]; cpu_jit.py:48-87 / model.py:229-301. */
+/* First tree level fused with the products: prod[j] = w[2j]*x[2j] + w[2j+1]*x[2j+1]
+ * (each product and the sum rounded separately -- the same values the
+ * reference's product pass + first _tree_reduce pass produce), odd tail
+ * carried; returns the width of the next level.  x is the contiguous m_x. */
+#if defined(__GNUC__) && defined(__x86_64__) && !defined(__clang__)
+__attribute__((target_clones("avx2", "default")))
+#endif
+static int64_t products_level1(const double *restrict wr, const double *restrict x,
+                               double *restrict prod, int64_t n) {
+    const int64_t half = n / 2;
+    for (int64_t j = 0; j < half; ++j) prod[j] = wr[2 * j] * x[2 * j] + wr[2 * j + 1] * x[2 * j + 1];
+    if (n & 1) {
+        prod[half] = wr[n - 1] * x[n - 1];
+        return half + 1;
+    }
+    return half;
+}
+
+/* dm/dt of oscillator k into out[3k..3k+2]; cpu_jit.py:48-87 / model.py:229-301.
+ * mx = the contiguous x-components of m (gathered once per derivative). */
 static void row_rhs(int64_t n, int64_t n_in, const double *w_cp, const double *w_in,
-                    const double *m, const double *u, double *out, double *prod_cp,
-                    double *prod_in, int64_t k, const consts_t *c) {
+                    const double *m, const double *mx_all, const double *u, double *out,
+                    double *prod_cp, double *prod_in, int64_t k, const consts_t *c) {
     const double *wr = w_cp + k * n;
-    for (int64_t j = 0; j < n; ++j) prod_cp[j] = wr[j] * m[3 * j];
-    double cp = sto_oracle_tree_sum(prod_cp, n);
+    double cp = sto_oracle_tree_sum(prod_cp, products_level1(wr, mx_all, prod_cp, n));
     const double *wi = w_in + k * n_in;
     for (int64_t j = 0; j < n_in; ++j) prod_in[j] = wi[j] * u[j];
     double cin = sto_oracle_tree_sum(prod_in, n_in);
@@ -98,13 +116,20 @@ typedef struct {
     const double *w_cp, *w_in;
     consts_t c;
     double *scratch; /* nthreads x (n + n_in) */
+    double *mx;      /* n: contiguous m_x of the current stage */
     int threads;
 } ctx_t;
 
-static void derivative(const ctx_t *x, const double *m, const double *u, double *out) {
+/* One derivative (cpu_jit.py:101-115: 128 fixed row blocks, so the thread
+ * count never changes bits).  Called by EVERY thread of an enclosing parallel
+ * region (or outside one): gathers m_x, then the row blocks; both worksharing
+ * loops end in an implicit barrier. */
+static void derivative_in_team(const ctx_t *x, const double *m, const double *u, double *out) {
     const int64_t n = x->n, n_in = x->n_in;
     const int64_t chunk = (n + ORACLE_ROW_BLOCKS - 1) / ORACLE_ROW_BLOCKS;
-#pragma omp parallel for schedule(static) num_threads(x->threads) if (x->threads > 1)
+#pragma omp for schedule(static)
+    for (int64_t j = 0; j < n; ++j) x->mx[j] = m[3 * j];
+#pragma omp for schedule(static)
     for (int b = 0; b < ORACLE_ROW_BLOCKS; ++b) {
         int tid = 0;
 #ifdef _OPENMP
@@ -114,8 +139,13 @@ static void derivative(const ctx_t *x, const double *m, const double *u, double 
         double *prod_in = prod_cp + n;
         int64_t lo = (int64_t)b * chunk, hi = lo + chunk < n ? lo + chunk : n;
         for (int64_t k = lo; k < hi; ++k)
-            row_rhs(n, n_in, x->w_cp, x->w_in, m, u, out, prod_cp, prod_in, k, &x->c);
+            row_rhs(n, n_in, x->w_cp, x->w_in, m, x->mx, u, out, prod_cp, prod_in, k, &x->c);
     }
+}
+
+static void derivative(const ctx_t *x, const double *m, const double *u, double *out) {
+#pragma omp parallel num_threads(x->threads) if (x->threads > 1)
+    derivative_in_team(x, m, u, out);
 }
 
 static int ctx_init(ctx_t *x, int64_t n, int64_t n_in, const double *w_cp,
@@ -127,7 +157,8 @@ static int ctx_init(ctx_t *x, int64_t n, int64_t n_in, const double *w_cp,
     x->w_in = w_in;
     x->c = unpack(consts);
     x->threads = threads;
-    x->scratch = (double *)malloc(sizeof(double) * (size_t)threads * (size_t)(n + n_in));
+    x->scratch = (double *)malloc(sizeof(double) * ((size_t)threads * (size_t)(n + n_in) + (size_t)n));
+    x->mx = x->scratch ? x->scratch + (size_t)threads * (size_t)(n + n_in) : NULL;
     return x->scratch ? 0 : -1;
 }
 
@@ -173,17 +204,25 @@ int sto_oracle_integrate(int64_t n, int64_t n_in, const double *w_cp, const doub
     int rc = STO_ORACLE_OK;
     int64_t rec = 1;
     memcpy(states, m, sizeof(double) * sz);
+    const int64_t isz = (int64_t)sz;
+    /* one parallel region for the whole run (no fork/join per derivative); the
+     * element-wise RK4 updates are worksharing loops -- same values per index */
+#pragma omp parallel num_threads(x.threads) if (x.threads > 1)
     for (int64_t step = 1; step <= steps; ++step) {
         const double *u =
             samples + (n_samples == 1 ? 0 : ((step - 1) / steps_per_sample)) * n_in;
-        derivative(&x, m, u, k1);
-        for (size_t i = 0; i < sz; ++i) s[i] = m[i] + k1[i] * h2;
-        derivative(&x, s, u, k2);
-        for (size_t i = 0; i < sz; ++i) s[i] = m[i] + k2[i] * h2;
-        derivative(&x, s, u, k3);
-        for (size_t i = 0; i < sz; ++i) s[i] = m[i] + k3[i] * dt;
-        derivative(&x, s, u, k4);
-        for (size_t i = 0; i < sz; ++i) {
+        derivative_in_team(&x, m, u, k1);
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < isz; ++i) s[i] = m[i] + k1[i] * h2;
+        derivative_in_team(&x, s, u, k2);
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < isz; ++i) s[i] = m[i] + k2[i] * h2;
+        derivative_in_team(&x, s, u, k3);
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < isz; ++i) s[i] = m[i] + k3[i] * dt;
+        derivative_in_team(&x, s, u, k4);
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < isz; ++i) {
             double t1 = k1[i] + k2[i] * 2.0;
             double t2 = k3[i] * 2.0 + k4[i];
             t1 = t1 + t2;
@@ -191,15 +230,19 @@ int sto_oracle_integrate(int64_t n, int64_t n_in, const double *w_cp, const doub
             m[i] = m[i] + t1;
         }
         if (step % stride == 0 || step == steps) {
-            int64_t bad = first_nonfinite_row(n, m);
-            if (bad >= 0) {
-                if (bad_oscillator) *bad_oscillator = bad;
-                if (bad_step) *bad_step = step;
-                rc = STO_ORACLE_E_DIVERGED;
-                break;
-            }
-            memcpy(states + (size_t)rec * sz, m, sizeof(double) * sz);
-            ++rec;
+#pragma omp single
+            {
+                int64_t bad = first_nonfinite_row(n, m);
+                if (bad >= 0) {
+                    if (bad_oscillator) *bad_oscillator = bad;
+                    if (bad_step) *bad_step = step;
+                    rc = STO_ORACLE_E_DIVERGED;
+                } else {
+                    memcpy(states + (size_t)rec * sz, m, sizeof(double) * sz);
+                    ++rec;
+                }
+            } /* implicit barrier: every thread sees rc */
+            if (rc != STO_ORACLE_OK) break;
         }
     }
     free(buf);
