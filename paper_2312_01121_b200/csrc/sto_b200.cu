@@ -326,6 +326,7 @@ template <int T, int C>
 int launch_clu_t(const KParams &p, int K, int threads, size_t smem, cudaStream_t stream) {
     auto fn = clu_rk4_kernel<T, C>;
     STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (K > 8) STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(K);
     cfg.blockDim = dim3(threads);
@@ -340,6 +341,39 @@ int launch_clu_t(const KParams &p, int K, int threads, size_t smem, cudaStream_t
     cfg.numAttrs = 1;
     STO_CUDA(cudaLaunchKernelEx(&cfg, fn, p));
     return STO_OK;
+}
+
+// clusters of K CTAs of the cluster kernel that can be resident at once
+int clu_max_clusters(int team, int cols, int K, int threads, size_t smem) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(K);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    auto q = [&](auto fn) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+            (K > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) ||
+            cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) != cudaSuccess)
+            nc = 0;
+    };
+    if (cols == 32) {
+        if (team == 2) q(clu_rk4_kernel<2, 32>);
+        else if (team == 4) q(clu_rk4_kernel<4, 32>);
+        else q(clu_rk4_kernel<8, 32>);
+    } else {
+        if (team == 4) q(clu_rk4_kernel<4, 16>);
+        else if (team == 8) q(clu_rk4_kernel<8, 16>);
+        else q(clu_rk4_kernel<16, 16>);
+    }
+    cudaGetLastError();
+    return nc;
 }
 
 // (team T, columns per thread C) of the cluster kernel; P = T*C padded row
@@ -563,11 +597,13 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         // CTA b owns the SEG = P/K rows whose x positions are [b*SEG, (b+1)*SEG):
         // one owner warp per CTA (SEG <= 32), K a power of two.  Fastest measured
         // (tools/clu_sweep.py): P = 64 -> K = 2, C = 32; P = 128 -> K = 8, C = 16;
-        // P = 256 -> K = 8, C = 32
+        // P = 256 -> K = 16 (non-portable cluster size), C = 32
         int cols = pc == 128 ? 16 : 32;
         if (const char *e = getenv("STO_CLU_C")) cols = atoi(e) == 16 ? 16 : 32;
-        int K = pc == 64 ? 2 : 8;
+        int K = pc == 64 ? 2 : pc == 128 ? 8 : 16;
         if (const char *e = getenv("STO_CLU_K")) K = std::max(1, std::min(atoi(e), kCluMaxK));
+        if (K > 8 && clu_max_clusters(pc / cols, cols, K, clu_threads(pc / K, pc / cols), clu_smem_bytes(pc)) < 1)
+            K = 8;  // no GPC with 16 free SMs (e.g. a shared device): the portable size
         P->team = pc / cols;
         P->clu_cols = cols;
         P->grid = K;

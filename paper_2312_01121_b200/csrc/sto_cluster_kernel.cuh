@@ -1,5 +1,5 @@
 // sto_cluster_kernel.cuh -- small reservoirs (33 <= n <= 256): ONE thread-block
-// cluster of K CTAs (K <= 8, one per SM), W held in registers, the stage
+// cluster of K CTAs (K <= 16 -- 16 is B200's non-portable maximum -- one per SM), W held in registers, the stage
 // x-vector pushed into every CTA's shared memory with `st.async` (DSMEM).
 //
 // The single-CTA kernel spends ~1.1 k cycles per stage on the GEMV of all n
@@ -51,7 +51,7 @@
 
 namespace sto {
 
-constexpr int kCluMaxK = 8;
+constexpr int kCluMaxK = 16;  // > 8: non-portable cluster size (B200 allows 16)
 
 __device__ __forceinline__ uint32_t clu_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);

@@ -25,7 +25,7 @@ def _variants(n):
     out = []
     for c in (32, 16):
         t = pc // c
-        for k in (1, 2, 4, 8):
+        for k in (2, 4, 8, 16):
             seg = pc // k
             threads = 32 + 32 * (-(-seg * t // 32))
             if t <= 32 and seg <= 32 and threads <= (288 if c == 32 else 576):
@@ -78,7 +78,7 @@ def test_divergence_reported_by_every_cluster_size(monkeypatch, name):
 
     d = load_golden(name)
     top = sto.Topology(sto.CouplingMatrix(d["w"]), sto.InputWeights(d["w_in"]))
-    for k in (2, 4, 8):
+    for k in (2, 4, 8, 16):
         be = _backend(sto, top, monkeypatch, k, 32, consts=d["consts"])
         with pytest.raises(sto.IntegrationDivergedError) as info:
             be.integrate_run(d["m0"].copy(), d["samples"], int(d["steps_per_sample"]),
