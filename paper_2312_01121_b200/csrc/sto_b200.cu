@@ -119,7 +119,7 @@ __global__ void permute_rows_kernel(const double *__restrict__ src, long long ld
 }
 
 constexpr int kMaxFlags = 1024;
-constexpr int kClusterMaxN = 256;  // cluster kernel: W of n <= 256 fits 8 SMs' registers
+constexpr int kClusterMaxN = 512;  // cluster kernel: W of n <= 512 fits 16 SMs' registers
 
 // logical row-major (zero padded to np x np) copy of W from the device layout
 // Ensemble W in DMMA fragment order for row tiles of TR = 8U rows
@@ -363,7 +363,9 @@ int clu_max_clusters(int team, int cols, int K, int threads, size_t smem) {
             cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) != cudaSuccess)
             nc = 0;
     };
-    if (cols == 32) {
+    if (cols == 64) {
+        q(clu_rk4_kernel<8, 64>);
+    } else if (cols == 32) {
         if (team == 2) q(clu_rk4_kernel<2, 32>);
         else if (team == 4) q(clu_rk4_kernel<4, 32>);
         else q(clu_rk4_kernel<8, 32>);
@@ -378,6 +380,7 @@ int clu_max_clusters(int team, int cols, int K, int threads, size_t smem) {
 
 // (team T, columns per thread C) of the cluster kernel; P = T*C padded row
 int launch_clu(const KParams &p, int team, int cols, int K, int threads, size_t smem, cudaStream_t s) {
+    if (cols == 64) return launch_clu_t<8, 64>(p, K, threads, smem, s);
     if (cols == 32) {
         switch (team) {
             case 2: return launch_clu_t<2, 32>(p, K, threads, smem, s);
@@ -567,6 +570,33 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     const size_t single_smem = grid_smem(n, cs, cs.ldw, true);
     int pw = 32;
     while (pw < n) pw <<= 1;
+    // cluster kernel configuration (CTA b owns the SEG = P/K rows whose x positions
+    // are [b*SEG, (b+1)*SEG): one owner warp per CTA, SEG <= 32, K a power of two).
+    // Fastest measured (tools/clu_sweep.py): P = 64 -> K = 2, C = 32; P = 128 ->
+    // K = 8, C = 16; P = 256 -> K = 16, C = 32; P = 512 -> K = 16, C = 64.  K = 16 is
+    // B200's non-portable cluster size: when 16 SMs of one GPC are not free,
+    // P = 256 falls back to K = 8 and P = 512 does not fit (register kernel).
+    struct {
+        int pc = 0, cols = 0, K = 0, team = 0, rows = 0, threads = 0;
+        bool fits = false;
+    } clu;
+    if (n <= kClusterMaxN) {
+        clu.pc = std::max(pw, 64);
+        clu.cols = clu.pc == 128 ? 16 : clu.pc == 512 ? 64 : 32;
+        if (const char *e = getenv("STO_CLU_C")) clu.cols = atoi(e) == 16 ? 16 : atoi(e) == 64 ? 64 : 32;
+        clu.K = clu.pc == 64 ? 2 : clu.pc == 128 ? 8 : 16;
+        if (const char *e = getenv("STO_CLU_K")) clu.K = std::max(1, std::min(atoi(e), kCluMaxK));
+        clu.team = clu.pc / clu.cols;
+        if (clu.K > 8 && (clu.cols != 64 || clu.team == 8) &&
+            clu_max_clusters(clu.team, clu.cols, clu.K, clu_threads(clu.pc / clu.K, clu.team),
+                             clu_smem_bytes(clu.pc)) < 1)
+            clu.K = 8;
+        clu.rows = clu.pc / clu.K;
+        clu.threads = clu_threads(clu.rows, clu.team);
+        clu.fits = !(clu.K & (clu.K - 1)) && clu.rows <= 32 && clu.team >= 1 && clu.team <= 32 &&
+                   (clu.cols != 64 || clu.team == 8) && clu.threads <= (clu.cols == 16 ? 576 : 288);
+    }
+
     if (sharded) {
         // sharded plans always use the grid kernel (MULTI); rows = this shard
         const int g = std::min(P->sm_count, P->rows);
@@ -590,28 +620,17 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         P->grid = 1;
         P->threads = 32;
     } else if ((fl & STO_PLAN_FORCE_CLUSTER) ||
-               (!forced && !(fl & STO_PLAN_NO_CLUSTER) && n <= kClusterMaxN)) {
-        if (n > kClusterMaxN) return bail(fail(STO_E_PARAM, "cluster kernel needs n <= 256"));
+               (!forced && !(fl & STO_PLAN_NO_CLUSTER) && n <= kClusterMaxN && clu.fits)) {
+        if (!clu.fits)
+            return bail(fail(STO_E_PARAM, "cluster kernel does not fit (n <= 512, K a power of two, "
+                                          "P/K <= 32 rows per CTA, 16-CTA clusters resident for n > 256)"));
         P->kind = kCluster;
-        const int pc = std::max(pw, 64);  // padded row P = T*C: T = 2..8 with C = 32
-        // CTA b owns the SEG = P/K rows whose x positions are [b*SEG, (b+1)*SEG):
-        // one owner warp per CTA (SEG <= 32), K a power of two.  Fastest measured
-        // (tools/clu_sweep.py): P = 64 -> K = 2, C = 32; P = 128 -> K = 8, C = 16;
-        // P = 256 -> K = 16 (non-portable cluster size), C = 32
-        int cols = pc == 128 ? 16 : 32;
-        if (const char *e = getenv("STO_CLU_C")) cols = atoi(e) == 16 ? 16 : 32;
-        int K = pc == 64 ? 2 : pc == 128 ? 8 : 16;
-        if (const char *e = getenv("STO_CLU_K")) K = std::max(1, std::min(atoi(e), kCluMaxK));
-        if (K > 8 && clu_max_clusters(pc / cols, cols, K, clu_threads(pc / K, pc / cols), clu_smem_bytes(pc)) < 1)
-            K = 8;  // no GPC with 16 free SMs (e.g. a shared device): the portable size
-        P->team = pc / cols;
-        P->clu_cols = cols;
-        P->grid = K;
-        P->rows_cap = pc / K;
-        P->threads = clu_threads(P->rows_cap, P->team);
-        P->smem = clu_smem_bytes(pc);
-        if ((K & (K - 1)) || P->rows_cap > 32 || P->threads > (cols == 32 ? 288 : 576) || P->team > 32)
-            return bail(fail(STO_E_PARAM, "cluster kernel does not fit (K a power of two, P/K <= 32 rows per CTA)"));
+        P->team = clu.team;
+        P->clu_cols = clu.cols;
+        P->grid = clu.K;
+        P->rows_cap = clu.rows;
+        P->threads = clu.threads;
+        P->smem = clu_smem_bytes(clu.pc);
     } else if ((fl & STO_PLAN_FORCE_REG) || (!forced && !(fl & STO_PLAN_NO_REG) && n <= 1024)) {
         if (n > 1024) return bail(fail(STO_E_PARAM, "register-resident kernel needs n <= 1024"));
         P->kind = kReg;

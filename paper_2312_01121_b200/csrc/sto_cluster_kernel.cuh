@@ -1,4 +1,4 @@
-// sto_cluster_kernel.cuh -- small reservoirs (33 <= n <= 256): ONE thread-block
+// sto_cluster_kernel.cuh -- small reservoirs (33 <= n <= 512): ONE thread-block
 // cluster of K CTAs (K <= 16 -- 16 is B200's non-portable maximum -- one per SM), W held in registers, the stage
 // x-vector pushed into every CTA's shared memory with `st.async` (DSMEM).
 //
@@ -136,11 +136,11 @@ __device__ __forceinline__ int clu_col_at(int pos, int T, int C) {
     return jj * C + 2 * a + e;
 }
 
-// 32 W columns per thread need > 128 registers: those variants run <= 288 threads
+// 32 or 64 W columns per thread need > 128 registers: those variants run <= 288 threads
 template <int T, int C>
-__global__ void __launch_bounds__(C == 32 ? 288 : 576, 1) clu_rk4_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const __grid_constant__ KParams p) {
     constexpr int P = T * C;
-    constexpr int LV = (C == 32) ? 5 : 4;  // tree levels above the products
+    constexpr int LV = (C == 64) ? 6 : (C == 32) ? 5 : 4;  // tree levels above the products
     static_assert(T <= 32, "team butterfly stays inside one warp");
     extern __shared__ __align__(16) double smem[];
     double *xs = smem;        // [2][P] team-blocked x, double-buffered by stage parity

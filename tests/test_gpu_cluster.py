@@ -1,4 +1,4 @@
-"""Thread-block-cluster kernel (csrc/sto_cluster_kernel.cuh, 33 <= n <= 256 by
+"""Thread-block-cluster kernel (csrc/sto_cluster_kernel.cuh, 33 <= n <= 512 by
 default): every cluster size K and W-columns-per-thread split C must reproduce
 the pinned oracle BIT FOR BIT, including ragged row splits (n not a multiple
 of P/K, so pad slots fall in every CTA), multi-channel drives held over several steps, recording strides, and
@@ -23,12 +23,13 @@ def _variants(n):
     rows per CTA, one owner warp + SEG*T GEMV threads within the launch bound."""
     pc = max(64, 1 << (max(n, 1) - 1).bit_length())
     out = []
-    for c in (32, 16):
+    for c in (64, 32, 16):
         t = pc // c
         for k in (2, 4, 8, 16):
             seg = pc // k
             threads = 32 + 32 * (-(-seg * t // 32))
-            if t <= 32 and seg <= 32 and threads <= (288 if c == 32 else 576):
+            if (1 <= t <= 32 and seg <= 32 and threads <= (576 if c == 16 else 288)
+                    and (c != 64 or t == 8)):
                 out.append((k, c))
     return out
 
@@ -44,7 +45,8 @@ def _backend(sto, top, monkeypatch, k, c, params=None, consts=None):
     return be
 
 
-@pytest.mark.parametrize("n,n_in", [(33, 1), (64, 3), (100, 1), (129, 2), (200, 1), (256, 2)])
+@pytest.mark.parametrize("n,n_in", [(33, 1), (64, 3), (100, 1), (129, 2), (200, 1), (256, 2),
+                                     (257, 1), (400, 2), (512, 1)])
 def test_every_cluster_shape_bit_exact(monkeypatch, oracle_mod, n, n_in):
     """Rows are owned by x-position segments, so ragged n leaves pad slots in
     every CTA; all of them must still give the pinned tree's bits."""
@@ -107,7 +109,8 @@ def test_auto_selects_cluster_for_small_reservoirs():
     import paper_2312_01121_b200 as sto
     from paper_2312_01121_b200.backends.b200 import B200Backend
 
-    for n, want in [(32, "tiny"), (33, "cluster"), (256, "cluster"), (257, "reg")]:
+    for n, want in [(32, "tiny"), (33, "cluster"), (256, "cluster"), (257, "cluster"), (512, "cluster"),
+                    (513, "reg")]:
         g = np.random.default_rng(n)
         w = g.uniform(-1, 1, (n, n)) / np.sqrt(n)
         np.fill_diagonal(w, 0.0)
