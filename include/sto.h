@@ -87,7 +87,7 @@ typedef struct {
 #define STO_PLAN_NO_TINY        0x8  /* do not use the one-warp kernel for n<=32  */
 #define STO_PLAN_FORCE_REG      0x10 /* W register-resident teams (n <= 1024)     */
 #define STO_PLAN_NO_REG         0x20 /* do not use the register-resident kernel    */
-#define STO_PLAN_FORCE_CLUSTER  0x40 /* one thread-block cluster, DSMEM exchange (n <= 256) */
+#define STO_PLAN_FORCE_CLUSTER  0x40 /* one thread-block cluster, DSMEM exchange (n <= 512) */
 #define STO_PLAN_NO_CLUSTER     0x80 /* do not use the cluster kernel              */
 
 typedef struct {
@@ -170,7 +170,10 @@ STO_API int sto_integrate_ensemble(sto_plan *plan, const sto_ensemble_run *run,
  * run->m must hold the full (n, 3) initial state on every rank; on return it
  * holds this rank's rows of the final state, and states (n_records, n, 3)
  * this rank's rows.  All ranks must call sto_integrate with the same run
- * parameters, and finish a run before any rank starts the next one. */
+ * parameters, and finish a run before any rank starts the next one.  A rank
+ * whose peer does not raise its epoch flag within STO_PEER_TIMEOUT_S seconds
+ * (default 120; the peer died or never launched) stops the run and returns
+ * STO_E_CUDA (status needed); the plan then refuses further runs. */
 STO_API int sto_plan_exchange_handle(sto_plan *plan, void *handle_out, int64_t handle_bytes);
 STO_API int sto_plan_connect(sto_plan *plan, const void *handles, int32_t world);
 
