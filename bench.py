@@ -114,7 +114,7 @@ def cached_topology(n: int, seed: int = 0):
             pass
     top = sto.build_topology(n, n_in=1, seed=seed)
     try:
-        tmp = cache.with_suffix(".tmp.npz")
+        tmp = cache.with_suffix(f".tmp{os.getpid()}.npz")  # torchrun ranks write concurrently
         np.savez(tmp, w=top.coupling.entries, w_in=top.input_weights.entries)
         os.replace(tmp, cache)
     except OSError:
