@@ -143,8 +143,21 @@ static void derivative_in_team(const ctx_t *x, const double *m, const double *u,
     }
 }
 
+/* Single-thread derivative with no OpenMP constructs (their per-call cost
+ * dominates at small n): the same rows in the same order. */
+static void derivative_serial(const ctx_t *x, const double *m, const double *u, double *out) {
+    const int64_t n = x->n, n_in = x->n_in;
+    for (int64_t j = 0; j < n; ++j) x->mx[j] = m[3 * j];
+    for (int64_t k = 0; k < n; ++k)
+        row_rhs(n, n_in, x->w_cp, x->w_in, m, x->mx, u, out, x->scratch, x->scratch + n, k, &x->c);
+}
+
 static void derivative(const ctx_t *x, const double *m, const double *u, double *out) {
-#pragma omp parallel num_threads(x->threads) if (x->threads > 1)
+    if (x->threads == 1) {
+        derivative_serial(x, m, u, out);
+        return;
+    }
+#pragma omp parallel num_threads(x->threads)
     derivative_in_team(x, m, u, out);
 }
 
@@ -205,9 +218,43 @@ int sto_oracle_integrate(int64_t n, int64_t n_in, const double *w_cp, const doub
     int64_t rec = 1;
     memcpy(states, m, sizeof(double) * sz);
     const int64_t isz = (int64_t)sz;
+    if (x.threads == 1) { /* serial: no OpenMP constructs on the small-n path */
+        for (int64_t step = 1; step <= steps; ++step) {
+            const double *u =
+                samples + (n_samples == 1 ? 0 : ((step - 1) / steps_per_sample)) * n_in;
+            derivative_serial(&x, m, u, k1);
+            for (int64_t i = 0; i < isz; ++i) s[i] = m[i] + k1[i] * h2;
+            derivative_serial(&x, s, u, k2);
+            for (int64_t i = 0; i < isz; ++i) s[i] = m[i] + k2[i] * h2;
+            derivative_serial(&x, s, u, k3);
+            for (int64_t i = 0; i < isz; ++i) s[i] = m[i] + k3[i] * dt;
+            derivative_serial(&x, s, u, k4);
+            for (int64_t i = 0; i < isz; ++i) {
+                double t1 = k1[i] + k2[i] * 2.0;
+                double t2 = k3[i] * 2.0 + k4[i];
+                t1 = t1 + t2;
+                t1 = t1 * dt_6;
+                m[i] = m[i] + t1;
+            }
+            if (step % stride == 0 || step == steps) {
+                int64_t bad = first_nonfinite_row(n, m);
+                if (bad >= 0) {
+                    if (bad_oscillator) *bad_oscillator = bad;
+                    if (bad_step) *bad_step = step;
+                    rc = STO_ORACLE_E_DIVERGED;
+                    break;
+                }
+                memcpy(states + (size_t)rec * sz, m, sizeof(double) * sz);
+                ++rec;
+            }
+        }
+        free(buf);
+        free(x.scratch);
+        return rc;
+    }
     /* one parallel region for the whole run (no fork/join per derivative); the
      * element-wise RK4 updates are worksharing loops -- same values per index */
-#pragma omp parallel num_threads(x.threads) if (x.threads > 1)
+#pragma omp parallel num_threads(x.threads)
     for (int64_t step = 1; step <= steps; ++step) {
         const double *u =
             samples + (n_samples == 1 ? 0 : ((step - 1) / steps_per_sample)) * n_in;
