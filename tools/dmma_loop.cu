@@ -9,6 +9,9 @@
 #ifndef KPH
 #define KPH 3
 #endif
+#ifndef NT
+#define NT 1  // member tiles (B fragments) per warp: U x NT DMMAs share U A- and NT B-fragments
+#endif
 constexpr int U = 7, KC = KCH, NK = KC / 4, WSL = 8 * U * KC, XSL = KC * 32, RING = 3;
 template <int MODE>  // 0 plain, 1 + syncwarp/atomic, 2 + mbarrier try_wait, 3 + double buffer off,
                      // 4 = 2 + real ring: the last warp refills the slot by bulk async copy from L2
@@ -35,8 +38,8 @@ __global__ void __launch_bounds__(640, 1) loop(int chunks, double *out, int warp
     if (MODE == 4 && threadIdx.x < RING) refill(threadIdx.x, threadIdx.x);
     if (warp >= warps_gemm) return;
     unsigned ph = 0;
-    const int mu = warp & 3, kph = (warp >> 2) % KPH;
-    double acc[U][2] = {};
+    const int mu = (warp % (4 / NT)) * NT, kph = (warp / (4 / NT)) % KPH;
+    double acc[U][NT][2] = {};
     int s = 0;
     for (int ch = 0; ch < chunks; ++ch) {
         if (MODE >= 2) {
@@ -55,25 +58,29 @@ __global__ void __launch_bounds__(640, 1) loop(int chunks, double *out, int warp
 #pragma unroll
                 for (int r = 0; r < U; ++r)
                     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                 : "+d"(acc[r][0]), "+d"(acc[r][1]) : "d"(a[r]), "d"(b));
+                                 : "+d"(acc[r][0][0]), "+d"(acc[r][0][1]) : "d"(a[r]), "d"(b));
             }
         } else {
-            double a[2][U], bf[2];
+            double a[2][U], bf[2][NT];
 #pragma unroll
             for (int r = 0; r < U; ++r) a[0][r] = W[(r * NK + kph) * 32 + lane];
-            bf[0] = X[(kph * 4 + mu) * 32 + lane];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) bf[0][t] = X[(kph * 4 + mu + t) * 32 + lane];
 #pragma unroll
             for (int q = 0; q < NK / KPH; ++q) {
                 if (q + 1 < NK / KPH) {
                     const int kn = KPH * (q + 1) + kph;
 #pragma unroll
                     for (int r = 0; r < U; ++r) a[(q + 1) & 1][r] = W[(r * NK + kn) * 32 + lane];
-                    bf[(q + 1) & 1] = X[(kn * 4 + mu) * 32 + lane];
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) bf[(q + 1) & 1][t] = X[(kn * 4 + mu + t) * 32 + lane];
                 }
 #pragma unroll
-                for (int r = 0; r < U; ++r)
-                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                 : "+d"(acc[r][0]), "+d"(acc[r][1]) : "d"(a[q & 1][r]), "d"(bf[q & 1]));
+                for (int t = 0; t < NT; ++t)
+#pragma unroll
+                    for (int r = 0; r < U; ++r)
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                     : "+d"(acc[r][t][0]), "+d"(acc[r][t][1]) : "d"(a[q & 1][r]), "d"(bf[q & 1][t]));
             }
         }
         if (MODE >= 1) {
@@ -90,7 +97,9 @@ __global__ void __launch_bounds__(640, 1) loop(int chunks, double *out, int warp
     }
     double t = 0;
 #pragma unroll
-    for (int r = 0; r < U; ++r) t += acc[r][0] + acc[r][1];
+    for (int r = 0; r < U; ++r)
+#pragma unroll
+        for (int u = 0; u < NT; ++u) t += acc[r][u][0] + acc[r][u][1];
     out[blockIdx.x * blockDim.x + threadIdx.x] = t;
 }
 template <int MODE>
@@ -108,8 +117,8 @@ void run(double *out, int sms, int threads, int gw, const double *src) {
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    const double flops = 512.0 * U * (NK / KPH) * chunks * gw * sms;
-    printf("mode %d threads %d gemm warps %d: %.2f TFLOP/s\n", MODE, threads, gw, flops / ms / 1e9);
+    const double flops = 512.0 * U * NT * (NK / KPH) * chunks * gw * sms;
+    printf("NT %d KPH %d mode %d threads %d gemm warps %d: %.2f TFLOP/s\n", NT, KPH, MODE, threads, gw, flops / ms / 1e9);
 }
 int main() {
     int sms;
@@ -119,7 +128,7 @@ int main() {
     double *src;
     cudaMalloc(&src, (size_t)200 * (WSL + XSL) * 8);
     cudaMemset(src, 0, (size_t)200 * (WSL + XSL) * 8);
-    for (int gw : {8, 12, 16}) {
+    for (int gw : {4, 8, 12, 16}) {
         run<0>(out, sms, 512, gw, src);
         run<4>(out, sms, 512, gw, src);
     }
