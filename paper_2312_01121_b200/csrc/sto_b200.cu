@@ -232,6 +232,7 @@ struct sto_plan {
     int team = 0;  // kReg: threads per row
     int rows_per_team = 1;
     int clu_cols = 0;  // kCluster: W columns per thread (grid = cluster size)
+    bool clu_hyb = true;  // kCluster: teams finish their rows (clu_hyb_kernel)
     // row sharding (world > 1)
     int world = 1, rank = 0;
     long long row_begin = 0;
@@ -323,8 +324,8 @@ int launch_reg_t(const RegParams &rp, int grid, int threads, size_t smem, cudaSt
 // one CTA; larger n uses C = 16 over the grid, R = 2 rows per team for the
 // 64-thread teams (each shared-memory x load then feeds two rows).
 template <int T, int C>
-int launch_clu_t(const KParams &p, int K, int threads, size_t smem, cudaStream_t stream) {
-    auto fn = clu_rk4_kernel<T, C>;
+int launch_clu_t(const KParams &p, bool hyb, int K, int threads, size_t smem, cudaStream_t stream) {
+    auto fn = hyb ? clu_hyb_kernel<T, C> : clu_rk4_kernel<T, C>;
     STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (K > 8) STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
@@ -344,7 +345,7 @@ int launch_clu_t(const KParams &p, int K, int threads, size_t smem, cudaStream_t
 }
 
 // clusters of K CTAs of the cluster kernel that can be resident at once
-int clu_max_clusters(int team, int cols, int K, int threads, size_t smem) {
+int clu_max_clusters(bool hyb, int team, int cols, int K, int threads, size_t smem) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(K);
     cfg.blockDim = dim3(threads);
@@ -363,35 +364,38 @@ int clu_max_clusters(int team, int cols, int K, int threads, size_t smem) {
             cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) != cudaSuccess)
             nc = 0;
     };
+#define STO_CLU_Q(T_, C_) q(hyb ? clu_hyb_kernel<T_, C_> : clu_rk4_kernel<T_, C_>)
     if (cols == 64) {
-        q(clu_rk4_kernel<8, 64>);
+        STO_CLU_Q(8, 64);
     } else if (cols == 32) {
-        if (team == 2) q(clu_rk4_kernel<2, 32>);
-        else if (team == 4) q(clu_rk4_kernel<4, 32>);
-        else q(clu_rk4_kernel<8, 32>);
+        if (team == 2) STO_CLU_Q(2, 32);
+        else if (team == 4) STO_CLU_Q(4, 32);
+        else STO_CLU_Q(8, 32);
     } else {
-        if (team == 4) q(clu_rk4_kernel<4, 16>);
-        else if (team == 8) q(clu_rk4_kernel<8, 16>);
-        else q(clu_rk4_kernel<16, 16>);
+        if (team == 4) STO_CLU_Q(4, 16);
+        else if (team == 8) STO_CLU_Q(8, 16);
+        else STO_CLU_Q(16, 16);
     }
+#undef STO_CLU_Q
     cudaGetLastError();
     return nc;
 }
 
 // (team T, columns per thread C) of the cluster kernel; P = T*C padded row
-int launch_clu(const KParams &p, int team, int cols, int K, int threads, size_t smem, cudaStream_t s) {
-    if (cols == 64) return launch_clu_t<8, 64>(p, K, threads, smem, s);
+int launch_clu(const KParams &p, bool hyb, int team, int cols, int K, int threads, size_t smem,
+               cudaStream_t s) {
+    if (cols == 64) return launch_clu_t<8, 64>(p, hyb, K, threads, smem, s);
     if (cols == 32) {
         switch (team) {
-            case 2: return launch_clu_t<2, 32>(p, K, threads, smem, s);
-            case 4: return launch_clu_t<4, 32>(p, K, threads, smem, s);
-            default: return launch_clu_t<8, 32>(p, K, threads, smem, s);
+            case 2: return launch_clu_t<2, 32>(p, hyb, K, threads, smem, s);
+            case 4: return launch_clu_t<4, 32>(p, hyb, K, threads, smem, s);
+            default: return launch_clu_t<8, 32>(p, hyb, K, threads, smem, s);
         }
     }
     switch (team) {
-        case 4: return launch_clu_t<4, 16>(p, K, threads, smem, s);
-        case 8: return launch_clu_t<8, 16>(p, K, threads, smem, s);
-        default: return launch_clu_t<16, 16>(p, K, threads, smem, s);
+        case 4: return launch_clu_t<4, 16>(p, hyb, K, threads, smem, s);
+        case 8: return launch_clu_t<8, 16>(p, hyb, K, threads, smem, s);
+        default: return launch_clu_t<16, 16>(p, hyb, K, threads, smem, s);
     }
 }
 
@@ -572,25 +576,35 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     while (pw < n) pw <<= 1;
     // cluster kernel configuration (CTA b owns the SEG = P/K rows whose x positions
     // are [b*SEG, (b+1)*SEG): one owner warp per CTA, SEG <= 32, K a power of two).
-    // Fastest measured (tools/clu_sweep.py): P = 64 -> K = 2, C = 32; P = 128 ->
-    // K = 8, C = 16; P = 256 -> K = 16, C = 32; P = 512 -> K = 16, C = 64.  K = 16 is
-    // B200's non-portable cluster size: when 16 SMs of one GPC are not free,
-    // P = 256 falls back to K = 8 and P = 512 does not fit (register kernel).
+    // Fastest measured (tools/clu_sweep.py, padded row P -> kernel, K, C):
+    //   P =  64 -> teams finish rows (clu_hyb_kernel), K = 2,  C = 32
+    //   P = 128 -> clu_hyb_kernel, K = 16, C = 32  (K = 8, C = 16 without 16-CTA clusters)
+    //   P = 256 -> owner warp (clu_rk4_kernel), K = 16, C = 32  (K = 8)
+    //   P = 512 -> clu_rk4_kernel, K = 16, C = 64  (register kernel without 16-CTA clusters)
+    // K = 16 is B200's non-portable cluster size: it needs 16 free SMs in one GPC.
     struct {
         int pc = 0, cols = 0, K = 0, team = 0, rows = 0, threads = 0;
-        bool fits = false;
+        bool fits = false, hyb = true;
     } clu;
     if (n <= kClusterMaxN) {
         clu.pc = std::max(pw, 64);
-        clu.cols = clu.pc == 128 ? 16 : clu.pc == 512 ? 64 : 32;
+        clu.hyb = clu.pc <= 128;
+        if (const char *e = getenv("STO_CLU_HYB")) clu.hyb = atoi(e) != 0;
+        clu.cols = clu.pc == 512 ? 64 : 32;
+        clu.K = clu.pc == 64 ? 2 : 16;
         if (const char *e = getenv("STO_CLU_C")) clu.cols = atoi(e) == 16 ? 16 : atoi(e) == 64 ? 64 : 32;
-        clu.K = clu.pc == 64 ? 2 : clu.pc == 128 ? 8 : 16;
         if (const char *e = getenv("STO_CLU_K")) clu.K = std::max(1, std::min(atoi(e), kCluMaxK));
         clu.team = clu.pc / clu.cols;
+        auto smem_of = [&] { return clu.hyb ? clu_hyb_smem_bytes(clu.pc) : clu_smem_bytes(clu.pc); };
         if (clu.K > 8 && (clu.cols != 64 || clu.team == 8) &&
-            clu_max_clusters(clu.team, clu.cols, clu.K, clu_threads(clu.pc / clu.K, clu.team),
-                             clu_smem_bytes(clu.pc)) < 1)
-            clu.K = 8;
+            clu_max_clusters(clu.hyb, clu.team, clu.cols, clu.K, clu_threads(clu.pc / clu.K, clu.team),
+                             smem_of()) < 1) {
+            clu.K = 8;  // the portable size
+            if (clu.pc == 128 && !getenv("STO_CLU_C")) {
+                clu.cols = 16;
+                clu.team = clu.pc / clu.cols;
+            }
+        }
         clu.rows = clu.pc / clu.K;
         clu.threads = clu_threads(clu.rows, clu.team);
         clu.fits = !(clu.K & (clu.K - 1)) && clu.rows <= 32 && clu.team >= 1 && clu.team <= 32 &&
@@ -630,7 +644,8 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         P->grid = clu.K;
         P->rows_cap = clu.rows;
         P->threads = clu.threads;
-        P->smem = clu_smem_bytes(clu.pc);
+        P->clu_hyb = clu.hyb;
+        P->smem = clu.hyb ? clu_hyb_smem_bytes(clu.pc) : clu_smem_bytes(clu.pc);
     } else if ((fl & STO_PLAN_FORCE_REG) || (!forced && !(fl & STO_PLAN_NO_REG) && n <= 1024)) {
         if (n > 1024) return bail(fail(STO_E_PARAM, "register-resident kernel needs n <= 1024"));
         P->kind = kReg;
@@ -803,7 +818,7 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
             break;
         }
         case kCluster:
-            rc = launch_clu(p, P->team, P->clu_cols, P->grid, P->threads, P->smem, s);
+            rc = launch_clu(p, P->clu_hyb, P->team, P->clu_cols, P->grid, P->threads, P->smem, s);
             break;
         case kSingle: rc = launch_grid<WSrc::Shared, true>(p, 1, P->smem, false, s); break;
         case kResident: rc = launch_grid<WSrc::Shared, false>(p, P->grid, P->smem, true, s); break;

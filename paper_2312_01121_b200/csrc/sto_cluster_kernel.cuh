@@ -371,4 +371,241 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
     clu_sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
+
+// ----------------------------------------------------------------------------
+// Hybrid variant (STO_CLU_HYB): the GEMV teams themselves finish their rows.
+// The xor butterfly leaves the row sum in every lane of the team, so every
+// lane runs the cp-dependent RHS half and the RK4 update of its row (the RK
+// state is replicated across the team's lanes, SIMT: no extra issue) and lane
+// j sends the new x to CTAs j, j + T, ...  The owner warp keeps only the
+// own-state half of the next stage's RHS (IEEE division included): lane 0 of
+// each team hands it the new stage point s (or m) through shared memory
+// (named barrier 4), it computes pre(s) while the x exchange and the next GEMV
+// run, and hands pre back (named barrier 3) before the teams need it.  The
+// per-stage critical path loses the row-sum and staging hand-offs of
+// clu_rk4_kernel: mbarrier wait -> GEMV + butterfly -> RHS post -> st.async.
+// ----------------------------------------------------------------------------
+__host__ __device__ constexpr size_t clu_hyb_smem_bytes(int P) {
+    return sizeof(double) * (2 * (size_t)P + 32 * 3 + 32 * 8) + 2 * sizeof(unsigned long long) + 16;
+}
+
+template <int T, int C>
+__global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const __grid_constant__ KParams p) {
+    constexpr int P = T * C;
+    constexpr int LV = (C == 64) ? 6 : (C == 32) ? 5 : 4;
+    static_assert(T <= 32, "team butterfly stays inside one warp");
+    extern __shared__ __align__(16) double smem[];
+    double *xs = smem;           // [2][P] team-blocked x, double-buffered by stage parity
+    double *sst = xs + 2 * P;    // [32][3] stage point, teams -> owner warp
+    double *spre = sst + 96;     // [32][8] own-state RHS half, owner warp -> teams
+    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(spre + 256);
+    volatile int *sbad = reinterpret_cast<volatile int *>(mbar + 2);
+
+    const int K = (int)clu_size(), b = (int)clu_rank();
+    const int n = p.rows;
+    const int SEG = P / K;
+    const bool gemv_warp = (int)threadIdx.x >= 32;
+    const int t = (int)threadIdx.x - 32;
+    const int row = gemv_warp ? t / T : 0, j = gemv_warp ? t % T : 0;
+    const int kg = (gemv_warp && row < SEG) ? clu_col_at(b * SEG + row, T, C) : n;  // team's oscillator
+    const int ko = (!gemv_warp && (int)threadIdx.x < SEG) ? clu_col_at(b * SEG + threadIdx.x, T, C) : n;
+    const unsigned nthreads = blockDim.x;
+
+    double w[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        const int col = j * C + q;
+        w[q] = (kg < n && col < n) ? p.w[(size_t)kg * p.cs.ldw + col_perm(p.cs, col)] : -0.0;
+    }
+    for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) xs[i] = 0.0;
+    __syncthreads();
+    for (int col = threadIdx.x; col < n; col += blockDim.x) xs[reg_xpos<C>(col, T)] = p.m[3 * (size_t)col];
+    const uint32_t bar0 = clu_u32(mbar), bar1 = clu_u32(mbar + 1);
+    if (threadIdx.x == 0) {
+        clu_bar_init(bar0, 1);
+        clu_bar_init(bar1, 1);
+        *sbad = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    clu_sync();  // every CTA's mbarriers and buffers are initialised before any st.async
+    const uint32_t xbytes = 8u * (uint32_t)n;
+    auto u_of = [&](long long st) {  // drive sample of step `st` (zero-order hold, model.py:93-149)
+        return p.n_samples > 1 ? p.samples + ((st - 1) / p.sps) * p.n_in : p.samples;
+    };
+    bool stop = false;
+
+    if (gemv_warp) {
+        // ==================== teams: GEMV, RHS post, RK4 update, publication ====
+        const bool live = kg < n;
+        V3 m{0.0, 0.0, 0.0}, s{0.0, 0.0, 0.0}, acc{0.0, 0.0, 0.0}, k3{0.0, 0.0, 0.0};
+        if (live) {
+            m = V3{p.m[3 * (size_t)kg], p.m[3 * (size_t)kg + 1], p.m[3 * (size_t)kg + 2]};
+            if (p.states && j == 0) {
+                double *st = p.states + 3 * (size_t)kg;
+                st[0] = m.x;
+                st[1] = m.y;
+                st[2] = m.z;
+            }
+        }
+        const uint32_t xa0 = clu_u32(xs + b * SEG + row), xa1 = clu_u32(xs + P + b * SEG + row);
+        if (t == 0) clu_expect(bar1, xbytes);  // x of stage 1
+        long long next_rec = p.stride, rec_idx = 1;
+        for (long long step = 1; step <= p.steps && !stop; ++step) {
+            const bool record = (step == next_rec) || (step == p.steps);
+#pragma unroll
+            for (int stage = 0; stage < 4; ++stage) {
+                const long long estage = (step - 1) * 4 + stage;
+                const int buf = stage & 1;
+                if (!(step == 1 && stage == 0)) {
+                    clu_wait(buf ? bar1 : bar0, (stage == 1 || stage == 2) ? 0u : 1u);
+                    if (t == 0) clu_expect(buf ? bar0 : bar1, xbytes);
+                }
+                CTL(estage, 3, t == 0, 0.0);
+                const double *xb = xs + buf * P;
+                double lvl[LV];
+#pragma unroll
+                for (int i = 0; i < C / 2; ++i) {
+                    const double2 x2 = *reinterpret_cast<const double2 *>(xb + ((i * T + j) << 1));
+                    double node = radd(rmul(w[2 * i], x2.x), rmul(w[2 * i + 1], x2.y));
+#pragma unroll
+                    for (int l = 0; l < LV - 1; ++l) {
+                        if (i & (1 << l)) node = radd(lvl[l], node);
+                        else { lvl[l] = node; break; }
+                    }
+                    if (i == C / 2 - 1) lvl[LV - 1] = node;
+                }
+                double cp = lvl[LV - 1];
+#pragma unroll
+                for (int mask = 1; mask < T; mask <<= 1) cp = radd(cp, __shfl_xor_sync(0xffffffffu, cp, mask));
+                CTL(estage, 4, t == 0, cp);
+                // own-state half of this stage's RHS, computed by the owner warp
+                asm volatile("bar.sync 3, %0;" ::"r"(nthreads) : "memory");
+                RhsPre pre;
+                {
+                    const double *q = spre + 8 * (row < SEG ? row : 0);
+                    const double2 a = *reinterpret_cast<const double2 *>(q);
+                    const double2 c2 = *reinterpret_cast<const double2 *>(q + 2);
+                    const double2 e = *reinterpret_cast<const double2 *>(q + 4);
+                    const double2 f = *reinterpret_cast<const double2 *>(q + 6);
+                    pre.m = V3{a.x, a.y, c2.x};
+                    pre.hs_qx = c2.y;
+                    pre.by = e.x;
+                    pre.bz = e.y;
+                    pre.ax = f.x;
+                    pre.ain_cin = f.y;
+                }
+                const V3 d = row_rhs_post(pre, cp, p.c);
+                double xpub;
+                bool bad = false;
+                if (stage == 0) {
+                    acc = d;
+                    s = stage_point(m, d, p.h2);
+                    xpub = s.x;
+                } else if (stage == 1) {
+                    acc = acc_k2(acc, d);
+                    s = stage_point(m, d, p.h2);
+                    xpub = s.x;
+                } else if (stage == 2) {
+                    k3 = d;
+                    s = stage_point(m, d, p.dt);
+                    xpub = s.x;
+                } else {
+                    m = rk4_final(m, acc, k3, d, p.dt6);
+                    xpub = m.x;
+                    if (record && live) {
+                        if (!all_finite(m)) {
+                            bad = true;
+                            if (j == 0) report_divergence(p.status, step, kg);
+                        } else if (p.states && j == 0) {
+                            const long long ri = (step == next_rec) ? rec_idx : p.n_records - 1;
+                            double *st = p.states + ((size_t)ri * n + kg) * 3;
+                            st[0] = m.x;
+                            st[1] = m.y;
+                            st[2] = m.z;
+                        }
+                    }
+                }
+                CTL(estage, 1, t == 0, xpub);
+                if (stage == 3 && record) {  // cluster-wide stop decision (uniform branch)
+                    if (bad) *sbad = 1;
+                    clu_sync();
+                    const uint32_t fl = clu_u32((const void *)sbad);
+                    for (int c = 0; c < K; ++c) stop |= clu_ld_s32(clu_mapa(fl, c)) != 0;
+                    if (stop) break;
+                }
+                if (!((step == p.steps) && stage == 3)) {
+                    const int nb = (stage + 1) & 1;
+                    if (live)
+                        for (int c = j; c < K; c += T)
+                            clu_st_async(clu_mapa(nb ? xa1 : xa0, c), xpub, clu_mapa(nb ? bar1 : bar0, c));
+                    // the new stage point (m after stage 3) to the owner warp
+                    if (j == 0 && row < SEG) {
+                        const V3 v = stage < 3 ? s : m;
+                        sst[3 * row] = v.x;
+                        sst[3 * row + 1] = v.y;
+                        sst[3 * row + 2] = v.z;
+                    }
+                    CTL(estage, 2, t == 0, 0.0);
+                    asm volatile("bar.arrive 4, %0;" ::"r"(nthreads) : "memory");
+                }
+            }
+            if (record && step == next_rec) {
+                next_rec += p.stride;
+                ++rec_idx;
+            }
+        }
+        if (live && j == 0) {
+            double *mm = p.m + 3 * (size_t)kg;
+            mm[0] = m.x;
+            mm[1] = m.y;
+            mm[2] = m.z;
+        }
+    } else {
+        // ==================== owner warp: own-state RHS half ==================
+        const int r = threadIdx.x;
+        const bool owner = ko < n;
+        const double win = (owner && p.n_in == 1) ? p.w_in[ko] : 0.0;
+        auto cin_of = [&](long long st) {
+            return (p.n_in == 1) ? rmul(win, u_of(st)[0])
+                                 : (owner ? tree_dot_stream(p.w_in + (size_t)ko * p.n_in, u_of(st), p.n_in) : 0.0);
+        };
+        auto put = [&](const RhsPre &q) {
+            if (r < SEG) {
+                double *o = spre + 8 * r;
+                *reinterpret_cast<double2 *>(o) = make_double2(q.m.x, q.m.y);
+                *reinterpret_cast<double2 *>(o + 2) = make_double2(q.m.z, q.hs_qx);
+                *reinterpret_cast<double2 *>(o + 4) = make_double2(q.by, q.bz);
+                *reinterpret_cast<double2 *>(o + 6) = make_double2(q.ax, q.ain_cin);
+            }
+        };
+        V3 m0{0.0, 0.0, 0.0};
+        if (owner) m0 = V3{p.m[3 * (size_t)ko], p.m[3 * (size_t)ko + 1], p.m[3 * (size_t)ko + 2]};
+        double cin = cin_of(1), u_next = 0.0;
+        put(row_rhs_pre(m0, cin, p.c));
+        asm volatile("bar.arrive 3, %0;" ::"r"(nthreads) : "memory");
+        long long next_rec = p.stride;
+        for (long long step = 1; step <= p.steps && !stop; ++step) {
+            const bool record = (step == next_rec) || (step == p.steps);
+#pragma unroll
+            for (int stage = 0; stage < 4; ++stage) {
+                if (stage == 3 && record) {  // the teams' stop decision, same barrier
+                    clu_sync();
+                    const uint32_t fl = clu_u32((const void *)sbad);
+                    for (int c = 0; c < K; ++c) stop |= clu_ld_s32(clu_mapa(fl, c)) != 0;
+                    if (stop) break;
+                }
+                if ((step == p.steps) && stage == 3) break;
+                if (stage == 0 && p.n_in == 1 && step < p.steps) u_next = u_of(step + 1)[0];  // prefetch
+                asm volatile("bar.sync 4, %0;" ::"r"(nthreads) : "memory");
+                const V3 v = r < SEG ? V3{sst[3 * r], sst[3 * r + 1], sst[3 * r + 2]} : V3{0.0, 0.0, 0.0};
+                if (stage == 3) cin = p.n_in == 1 ? rmul(win, u_next) : cin_of(step + 1);
+                put(row_rhs_pre(v, cin, p.c));
+                asm volatile("bar.arrive 3, %0;" ::"r"(nthreads) : "memory");
+            }
+            if (record && step == next_rec) next_rec += p.stride;
+        }
+    }
+    clu_sync();  // no CTA leaves while a peer may still write its shared memory
+}
+
 }  // namespace sto

@@ -18,6 +18,14 @@ pytestmark = pytest.mark.gpu
 CLUSTER = 0x40 | 0x8  # STO_PLAN_FORCE_CLUSTER | STO_PLAN_NO_TINY
 
 
+@pytest.fixture(autouse=True, params=[1, 0], ids=["teams-finish-rows", "owner-warp"])
+def clu_variant(request, monkeypatch):
+    """Every test runs on both cluster kernels (STO_CLU_HYB): clu_hyb_kernel
+    (the teams run the RHS of their rows) and clu_rk4_kernel (owner warp)."""
+    monkeypatch.setenv("STO_CLU_HYB", str(request.param))
+    return request.param
+
+
 def _variants(n):
     """(K, C) pairs the host accepts (sto_b200.cu): K a power of two, SEG = P/K <= 32
     rows per CTA, one owner warp + SEG*T GEMV threads within the launch bound."""

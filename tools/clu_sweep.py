@@ -26,11 +26,13 @@ for n in ns:
     samples = g.uniform(-1, 1, (19, n_in))
     want, _ = oracle.integrate(w, w_in, sto.kernel_scalars(params), m0, samples, 3, 1e-11, 57, 4)
     variants = [("reg", nat.FORCE_REG | nat.NO_TINY, {})]
-    for c in (64, 32, 16):
-        for k in (2, 4, 8, 16):
-            variants.append((f"clu K={k} C={c}", nat.FORCE_CLUSTER, {"STO_CLU_K": str(k), "STO_CLU_C": str(c)}))
+    for hyb in (1, 0):
+        for c in (64, 32, 16):
+            for k in (2, 4, 8, 16):
+                variants.append((f"{'hyb' if hyb else 'own'} K={k} C={c}", nat.FORCE_CLUSTER,
+                                 {"STO_CLU_K": str(k), "STO_CLU_C": str(c), "STO_CLU_HYB": str(hyb)}))
     for name, flags, env in variants:
-        for key in ("STO_CLU_K", "STO_CLU_C"):
+        for key in ("STO_CLU_K", "STO_CLU_C", "STO_CLU_HYB"):
             os.environ.pop(key, None)
         os.environ.update(env)
         try:
