@@ -27,6 +27,13 @@ for who in range(2):
     for s in range(16):
         row = t[who, s] - t0
         d = np.diff(t[who, s])
+        if be.plan_info["kernel_name"] == "cluster" and os.environ.get("STO_CLU_HYB", "1") != "0" and n <= 128:
+            # clu_hyb_kernel: 3 team got x, 4 butterfly done, 1 RHS post + update done, 2 published
+            nx = t[who, s + 1] if s < 15 else t[who, s] * np.nan
+            print(f"  stage {400+s}: cycle {nx[3] - t[who, s, 3]:6.0f}  gemv {t[who, s, 4] - t[who, s, 3]:5.0f}  "
+                  f"post {t[who, s, 1] - t[who, s, 4]:5.0f}  publish {t[who, s, 2] - t[who, s, 1]:5.0f}  "
+                  f"exchange {nx[3] - t[who, s, 2]:6.0f}")
+            continue
         if be.plan_info["kernel_name"] == "cluster":
             # events: 0 owner has row sums, 1 post+update done, 2 published,
             #         3 GEMV warp got x, 4 GEMV butterfly done
