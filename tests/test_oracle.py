@@ -35,18 +35,21 @@ def test_derivatives_bit_exact(oracle_mod):
             assert_bit_equal(got, z[key + "_out"], f"derivative {key} threads={threads}")
 
 
+@pytest.mark.parametrize("threads", [1, 2], ids=["serial", "openmp"])
 @pytest.mark.parametrize("name", golden_trajectories())
-def test_trajectories_bit_exact(oracle_mod, name):
+def test_trajectories_bit_exact(oracle_mod, name, threads):
+    """Both oracle paths (single thread: no OpenMP constructs; several threads:
+    one parallel region per run) against the reference's own trajectories."""
     d = load_golden(name)
     args = (d["w"], d["w_in"], d["consts"], d["m0"], d["samples"],
             int(d["steps_per_sample"]), float(d["dt"]), int(d["steps"]), int(d["stride"]))
     if bool(d["diverged"]):
         with pytest.raises(oracle_mod.OracleDiverged) as info:
-            oracle_mod.integrate(*args, threads=2)
+            oracle_mod.integrate(*args, threads=threads)
         assert (info.value.oscillator, info.value.step) == (int(d["bad_oscillator"]),
                                                            int(d["bad_step"]))
         return
-    states, final = oracle_mod.integrate(*args, threads=2)
+    states, final = oracle_mod.integrate(*args, threads=threads)
     assert_bit_equal(states, d["states"], name)
     assert_bit_equal(final, d["states"][-1], name + " final")
 
