@@ -578,7 +578,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     // are [b*SEG, (b+1)*SEG): one owner warp per CTA, SEG <= 32, K a power of two).
     // Fastest measured (tools/clu_sweep.py, padded row P -> kernel, K, C):
     //   P =  64 -> teams finish rows (clu_hyb_kernel), K = 2,  C = 32
-    //   P = 128 -> clu_hyb_kernel, K = 16, C = 32  (K = 8, C = 16 without 16-CTA clusters)
+    //   P = 128 -> clu_hyb_kernel, K = 8,  C = 32
     //   P = 256 -> owner warp (clu_rk4_kernel), K = 16, C = 32  (K = 8)
     //   P = 512 -> clu_rk4_kernel, K = 16, C = 64  (register kernel without 16-CTA clusters)
     // K = 16 is B200's non-portable cluster size: it needs 16 free SMs in one GPC.
@@ -591,7 +591,7 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
         clu.hyb = clu.pc <= 128;
         if (const char *e = getenv("STO_CLU_HYB")) clu.hyb = atoi(e) != 0;
         clu.cols = clu.pc == 512 ? 64 : 32;
-        clu.K = clu.pc == 64 ? 2 : 16;
+        clu.K = clu.pc == 64 ? 2 : clu.pc == 128 ? 8 : 16;
         if (const char *e = getenv("STO_CLU_C")) clu.cols = atoi(e) == 16 ? 16 : atoi(e) == 64 ? 64 : 32;
         if (const char *e = getenv("STO_CLU_K")) clu.K = std::max(1, std::min(atoi(e), kCluMaxK));
         clu.team = clu.pc / clu.cols;
@@ -600,10 +600,6 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
             clu_max_clusters(clu.hyb, clu.team, clu.cols, clu.K, clu_threads(clu.pc / clu.K, clu.team),
                              smem_of()) < 1) {
             clu.K = 8;  // the portable size
-            if (clu.pc == 128 && !getenv("STO_CLU_C")) {
-                clu.cols = 16;
-                clu.team = clu.pc / clu.cols;
-            }
         }
         clu.rows = clu.pc / clu.K;
         clu.threads = clu_threads(clu.rows, clu.team);
