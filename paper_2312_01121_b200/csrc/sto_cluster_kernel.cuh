@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
     extern __shared__ __align__(16) double smem[];
     double *xs = smem;           // [2][P] team-blocked x, double-buffered by stage parity
     double *sst = xs + 2 * P;    // [32][3] stage point, teams -> owner warp
-    double *spre = sst + 96;     // [32][8] own-state RHS half, owner warp -> teams
+    double *spre = sst + 96;     // 256: own-state RHS half, owner warp -> teams ([8][32] if T <= 2, else [32][8])
     unsigned long long *mbar = reinterpret_cast<unsigned long long *>(spre + 256);
     volatile int *sbad = reinterpret_cast<volatile int *>(mbar + 2);
 
@@ -481,7 +481,18 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
                 // own-state half of this stage's RHS, computed by the owner warp
                 asm volatile("bar.sync 3, %0;" ::"r"(nthreads) : "memory");
                 RhsPre pre;
-                {
+                if constexpr (T <= 2) {
+                    // >= 16 rows per warp: field-major [8][32], a warp's rows read
+                    // consecutive words (row-major 64-byte records would conflict 8-way)
+                    const double *q = spre + (row < SEG ? row : 0);
+                    pre.m = V3{q[0], q[32], q[64]};
+                    pre.hs_qx = q[96];
+                    pre.by = q[128];
+                    pre.bz = q[160];
+                    pre.ax = q[192];
+                    pre.ain_cin = q[224];
+                } else {
+                    // <= 8 rows per warp: row-major [32][8], four 16-byte loads per lane
                     const double *q = spre + 8 * (row < SEG ? row : 0);
                     const double2 a = *reinterpret_cast<const double2 *>(q);
                     const double2 c2 = *reinterpret_cast<const double2 *>(q + 2);
@@ -571,11 +582,23 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
         };
         auto put = [&](const RhsPre &q) {
             if (r < SEG) {
-                double *o = spre + 8 * r;
-                *reinterpret_cast<double2 *>(o) = make_double2(q.m.x, q.m.y);
-                *reinterpret_cast<double2 *>(o + 2) = make_double2(q.m.z, q.hs_qx);
-                *reinterpret_cast<double2 *>(o + 4) = make_double2(q.by, q.bz);
-                *reinterpret_cast<double2 *>(o + 6) = make_double2(q.ax, q.ain_cin);
+                if constexpr (T <= 2) {
+                    double *o = spre + r;
+                    o[0] = q.m.x;
+                    o[32] = q.m.y;
+                    o[64] = q.m.z;
+                    o[96] = q.hs_qx;
+                    o[128] = q.by;
+                    o[160] = q.bz;
+                    o[192] = q.ax;
+                    o[224] = q.ain_cin;
+                } else {
+                    double *o = spre + 8 * r;
+                    *reinterpret_cast<double2 *>(o) = make_double2(q.m.x, q.m.y);
+                    *reinterpret_cast<double2 *>(o + 2) = make_double2(q.m.z, q.hs_qx);
+                    *reinterpret_cast<double2 *>(o + 4) = make_double2(q.by, q.bz);
+                    *reinterpret_cast<double2 *>(o + 6) = make_double2(q.ax, q.ain_cin);
+                }
             }
         };
         V3 m0{0.0, 0.0, 0.0};
