@@ -541,7 +541,8 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
     };
     cudaStream_t s = nullptr;
     const int n = P->n;
-    const int blk_hint = n >= 8192 ? 2048 : 512;
+    int blk_hint = n >= 8192 ? 2048 : 512;
+    if (const char *e = getenv("STO_BLK")) blk_hint = std::max(512, atoi(e));  // (row, block) unit width
     if (int rc = upload_layout(P->L, P->rows, n, d->w_cp, d->ld_cp, blk_hint, s)) return bail(rc);
     const ColSched &cs = P->L.cs;
     if (sharded) {
