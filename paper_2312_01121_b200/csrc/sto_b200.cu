@@ -232,6 +232,7 @@ struct sto_plan {
     int team = 0;  // kReg: threads per row
     int rows_per_team = 1;
     int clu_cols = 0;  // kCluster: W columns per thread (grid = cluster size)
+    int grid_threads = kThreads;  // kStream (HBM-streaming, unsharded): 512 or 544
     bool clu_hyb = true;  // kCluster: teams finish their rows (clu_hyb_kernel)
     // row sharding (world > 1)
     int world = 1, rank = 0;
@@ -269,19 +270,30 @@ int choose_chunk(const ColSched &cs, int rows_cap, bool resident) {
     return std::max(chunk, cs.blk);
 }
 
-template <WSrc S, bool SINGLE>
+template <WSrc S, bool SINGLE, int NT = kThreads>
 int launch_grid(const KParams &p, int grid, size_t smem, bool cooperative, cudaStream_t stream) {
-    auto fn = grid_rk4_kernel<S, SINGLE>;
+    auto fn = grid_rk4_kernel<S, SINGLE, false, NT>;
     STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (cooperative) {
         void *args[] = {(void *)&p};
-        STO_CUDA(cudaLaunchCooperativeKernel((void *)fn, dim3(grid), dim3(kThreads), args, smem,
+        STO_CUDA(cudaLaunchCooperativeKernel((void *)fn, dim3(grid), dim3(NT), args, smem,
                                              stream));
     } else {
-        fn<<<grid, kThreads, smem, stream>>>(p);
+        fn<<<grid, NT, smem, stream>>>(p);
         STO_CUDA(cudaGetLastError());
     }
     return STO_OK;
+}
+
+// Threads per CTA of the HBM-streaming kernel: 17 warps (544 threads, <= 96
+// registers) keep more 16-byte loads in flight per SM and split a CTA's
+// (row, block) units more finely; measured (tools/midsize_sweep.py, bench):
+// N = 5000 / 7000 / 1e4 +4.5 / +2 / +2 %, but -1 % at N = 4e4 where x is staged
+// in chunks.  So 544 when one x window covers the row, else 512.
+// STO_GRID_WARPS=16/17 forces either.
+int stream_threads(const ColSched &cs, int chunk_cols) {
+    if (const char *e = getenv("STO_GRID_WARPS")) return atoi(e) == 17 ? 544 : kThreads;
+    return chunk_cols >= cs.ldw ? 544 : kThreads;
 }
 
 template <WSrc S>
@@ -623,7 +635,10 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
             P->smem = grid_smem(P->rows_cap, cs, P->chunk_cols, false);
             const double wbytes = (double)P->rows * cs.ldw * sizeof(double);
             P->stream_evict_first = wbytes > 0.75 * (double)P->l2_bytes;
-            if (P->stream_evict_first) P->l2_keep_rows = l2_keep_rows_for(P->l2_bytes, g, cs.ldw);
+            if (P->stream_evict_first) {
+                P->l2_keep_rows = l2_keep_rows_for(P->l2_bytes, g, cs.ldw);
+                P->grid_threads = stream_threads(cs, P->chunk_cols);
+            }
         }
         P->grid = g;
     } else if (n <= 32 && !(fl & STO_PLAN_NO_TINY) && !forced) {
@@ -698,7 +713,10 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
             P->smem = grid_smem(P->rows_cap, cs, P->chunk_cols, false);
             const double wbytes = (double)n * cs.ldw * sizeof(double);
             P->stream_evict_first = wbytes > 0.75 * (double)P->l2_bytes;
-            if (P->stream_evict_first) P->l2_keep_rows = l2_keep_rows_for(P->l2_bytes, g, cs.ldw);
+            if (P->stream_evict_first) {
+                P->l2_keep_rows = l2_keep_rows_for(P->l2_bytes, g, cs.ldw);
+                P->grid_threads = stream_threads(cs, P->chunk_cols);
+            }
         }
         P->grid = g;
     }
@@ -731,7 +749,9 @@ int sto_plan_get_info(const sto_plan *P, sto_plan_info *info) {
     if (!P || !info) return fail(STO_E_PARAM, "null plan or info");
     info->kernel = P->kind;
     info->grid = P->grid;
-    info->threads = (P->kind == kTiny || P->kind == kReg || P->kind == kCluster) ? P->threads : kThreads;
+    info->threads = (P->kind == kTiny || P->kind == kReg || P->kind == kCluster) ? P->threads
+                    : P->kind == kStream                                          ? P->grid_threads
+                                                                                  : kThreads;
     info->smem_bytes = (int)P->smem;
     info->ldw = P->L.cs.ldw;
     info->block_cols = P->L.cs.blk;
@@ -821,7 +841,9 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
         case kResident: rc = launch_grid<WSrc::Shared, false>(p, P->grid, P->smem, true, s); break;
         default:
             rc = P->stream_evict_first
-                     ? launch_grid<WSrc::GlobalStream, false>(p, P->grid, P->smem, true, s)
+                     ? (P->grid_threads == 544
+                            ? launch_grid<WSrc::GlobalStream, false, 544>(p, P->grid, P->smem, true, s)
+                            : launch_grid<WSrc::GlobalStream, false>(p, P->grid, P->smem, true, s))
                      : launch_grid<WSrc::GlobalL2, false>(p, P->grid, P->smem, true, s);
     }
     if (rc) return rc;
