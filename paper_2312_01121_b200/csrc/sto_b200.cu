@@ -232,7 +232,7 @@ struct sto_plan {
     int team = 0;  // kReg: threads per row
     int rows_per_team = 1;
     int clu_cols = 0;  // kCluster: W columns per thread (grid = cluster size)
-    int grid_threads = kThreads;  // kStream (HBM-streaming, unsharded): 512 or 544
+    int grid_threads = kThreads;  // kStream (HBM-streaming, unsharded): 512 or 640
     bool clu_hyb = true;  // kCluster: teams finish their rows (clu_hyb_kernel)
     // row sharding (world > 1)
     int world = 1, rank = 0;
@@ -285,15 +285,17 @@ int launch_grid(const KParams &p, int grid, size_t smem, bool cooperative, cudaS
     return STO_OK;
 }
 
-// Threads per CTA of the HBM-streaming kernel: 17 warps (544 threads, <= 96
-// registers) keep more 16-byte loads in flight per SM and split a CTA's
-// (row, block) units more finely; measured (tools/midsize_sweep.py, bench):
-// N = 5000 / 7000 / 1e4 +4.5 / +2 / +2 %, but -1 % at N = 4e4 where x is staged
-// in chunks.  So 544 when one x window covers the row, else 512.
-// STO_GRID_WARPS=16/17 forces either.
+// Threads per CTA of the HBM-streaming kernel: 20 warps (640 threads, <= 96
+// registers) keep more 16-byte loads in flight per SM than 16; measured
+// (bench n1e4 on two boxes, tools/midsize_sweep.py), relative to 16 warps:
+//   warps   17     18     20     24     32
+//   n1e4  +1.5%  +2.5%  +3.7%  +2.6%  -1.2%   (N = 5000 / 7000 / 15000 at 20:
+//   +5.6 / +7.5 / +5.7 %, at 24 slightly more); N = 4e4, where x is staged in
+// chunks: within +-1 %.  So 640 when one x window covers the row, else 512.
+// STO_GRID_WARPS=16/20 forces either.
 int stream_threads(const ColSched &cs, int chunk_cols) {
-    if (const char *e = getenv("STO_GRID_WARPS")) return atoi(e) == 17 ? 544 : kThreads;
-    return chunk_cols >= cs.ldw ? 544 : kThreads;
+    if (const char *e = getenv("STO_GRID_WARPS")) return atoi(e) == 20 ? 640 : kThreads;
+    return chunk_cols >= cs.ldw ? 640 : kThreads;
 }
 
 template <WSrc S>
@@ -841,8 +843,8 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
         case kResident: rc = launch_grid<WSrc::Shared, false>(p, P->grid, P->smem, true, s); break;
         default:
             rc = P->stream_evict_first
-                     ? (P->grid_threads == 544
-                            ? launch_grid<WSrc::GlobalStream, false, 544>(p, P->grid, P->smem, true, s)
+                     ? (P->grid_threads == 640
+                            ? launch_grid<WSrc::GlobalStream, false, 640>(p, P->grid, P->smem, true, s)
                             : launch_grid<WSrc::GlobalStream, false>(p, P->grid, P->smem, true, s))
                      : launch_grid<WSrc::GlobalL2, false>(p, P->grid, P->smem, true, s);
     }

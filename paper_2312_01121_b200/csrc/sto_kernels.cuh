@@ -227,7 +227,7 @@ __device__ unsigned long long g_grid_cta_block[2][1024];  // per CTA: block-phas
 #endif
 
 // Shared layout: [X window | W rows (resident) | nodes | row state | flags]
-// NT threads per CTA: 512, or 544 (17 warps, <= 96 registers) for the unchunked
+// NT threads per CTA: 512, or 640 (20 warps, <= 96 registers) for the unchunked
 // HBM-streaming case (host: stream_threads)
 template <WSrc S, bool SINGLE, bool MULTI = false, int NT = 512>
 __global__ void __launch_bounds__(NT, 1) grid_rk4_kernel(const __grid_constant__ KParams p) {
