@@ -11,6 +11,6 @@ run n1e4 20 grid_rk4
 run n4e4 4 grid_rk4
 run n1000 2000 reg_rk4
 run ens512 200 ens_rk4
-run n100 2000 clu_rk4
+run n100 2000 clu_
 run n1 20000 tiny_rk4
 ls -la gpurun_out/traffic_*.csv
