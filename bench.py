@@ -565,6 +565,7 @@ def run_ours(args, rank, world, local_rank):
                                        if sharded else f"replicas x{world}" if world > 1
                                        else "1 GPU"),
                        "kernel": info["kernel_name"], "grid": info["grid"],
+                       "cta_threads": info.get("threads"),
                        "l2": ("inputs larger than L2 (W %.0f MB)" % (info["w_bytes"] / 1e6))
                        if info["w_bytes"] > 126e6 else
                        "W on-chip/L2-resident by design (persistent kernel; one launch per run)"},
