@@ -515,7 +515,9 @@ def run_ours(args, rank, world, local_rank):
     peaks = measured_peaks()
     alg_bytes = 32.0 * rows_mine * n * steps  # one f64 W row per RK stage per (own) osc-step
     achieved = alg_bytes / kernel_s / 1e9
-    kname = {"tiny": "tiny_rk4_kernel", "reg": "reg_rk4_kernel", "cluster": "clu_rk4_kernel",
+    clu_hyb = max(64, 1 << (n - 1).bit_length()) <= 128 and os.environ.get("STO_CLU_HYB") != "0"
+    kname = {"tiny": "tiny_rk4_kernel", "reg": "reg_rk4_kernel",
+             "cluster": "clu_hyb_kernel" if clu_hyb else "clu_rk4_kernel",
              "single": "grid_rk4_kernel[Shared,single]",
              "resident": "grid_rk4_kernel[Shared]",
              "stream": "grid_rk4_kernel[GlobalStream]"}.get(info["kernel_name"], info["kernel_name"])
@@ -524,6 +526,14 @@ def run_ours(args, rank, world, local_rank):
                 "traffic": traffic_per_launch(name, steps),
                 "peak_source": "fallback" if peaks.get("fallback") else "measured",
                 "kernel": kname}
+    if roofline["traffic"]:
+        share = roofline["traffic"] / (32.0 * rows_mine * n * steps)
+        if info["kernel_name"].startswith("stream") and share < 1.0:
+            roofline["note"] = ("achieved counts algorithmic W bytes; DRAM traffic is %.3f of them (a "
+                                "slice of W stays L2-resident across stages), so frac can exceed 1" % share)
+        elif info["kernel_name"] in ("reg", "resident"):
+            roofline["note"] = ("W is held on chip (registers / shared memory): HBM-equivalent roofline "
+                                "(SURVEY 8(d)); DRAM traffic is %.2g of the algorithmic bytes" % share)
     if n < 1000:
         # W is a few KB: no HBM/tensor roofline applies.  The bound is the dependent
         # fp64 chain of one RK4 step (4 RHS evaluations, DDIV included): 1125 cycles
