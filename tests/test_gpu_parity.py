@@ -205,3 +205,27 @@ def test_host_buffer_abi_entry_point(sto, oracle_mod):
     assert rc == 0, _native.last_error()
     assert_bit_equal(states, d["states"])
     assert_bit_equal(m, d["states"][-1])
+
+
+@pytest.mark.parametrize("warps", ["auto", "16", "20"])
+def test_streaming_warp_counts_bit_exact(sto, oracle_mod, monkeypatch, warps):
+    """The HBM-streaming kernel runs 20 warps per CTA when x fits one window
+    (host: stream_threads) and 16 otherwise; both counts split the same
+    (row, block) tree nodes, so the bits must not change (N = 5000, W 200 MB)."""
+    if warps != "auto":
+        monkeypatch.setenv("STO_GRID_WARPS", warps)
+    n = 5000
+    g = np.random.default_rng(5000)
+    w = g.uniform(-1, 1, (n, n)) / np.sqrt(n / 3.0)
+    np.fill_diagonal(w, 0.0)
+    w_in = g.uniform(-1, 1, (n, 1))
+    consts = sto.kernel_scalars(sto.PhysicalParams())
+    m0 = sto.initial_state(n)
+    samples = g.uniform(-1, 1, (4, 1))
+    want, _ = oracle_mod.integrate(w, w_in, consts, m0, samples, 1, 1e-11, 4, 2)
+    d = dict(w=w, w_in=w_in, consts=np.array(consts), m0=m0, samples=samples,
+             steps_per_sample=1, dt=1e-11, steps=4, stride=2)
+    states, _, info = _run(sto, d, "auto")
+    assert info["kernel_name"] == "stream"
+    assert info["threads"] == (512 if warps == "16" else 640), info
+    assert_bit_equal(states, want, f"n=5000 warps={warps}")
