@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define STO_ABI_VERSION 1
+#define STO_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define STO_API __attribute__((visibility("default")))
@@ -117,6 +117,8 @@ typedef struct {
     int64_t ldw;             /* padded row width of the device W layout              */
     int64_t block_cols;      /* columns per (row, block) work unit                   */
     int64_t w_bytes;         /* device bytes of the W layout                          */
+    int64_t x_window_cols;   /* columns of x staged per shared-memory window (== ldw
+                                unless the row is processed in several windows)     */
 } sto_plan_info;
 
 STO_API const char *sto_last_error(void);

@@ -64,7 +64,7 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("ldw", ctypes.c_int64), ("block_cols", ctypes.c_int64),
-                ("w_bytes", ctypes.c_int64)]
+                ("w_bytes", ctypes.c_int64), ("x_window_cols", ctypes.c_int64)]
 
 
 # every symbol include/sto.h declares, with its ctypes signature

@@ -93,6 +93,12 @@ class B200Backend:
         """Write dm/dt at (m, u) into `out` (numpy or CUDA torch tensors)."""
         t = self._torch
         if isinstance(m, t.Tensor) and m.is_cuda:
+            for a, shape in ((m, (self.n, 3)), (u, (self.n_in,)), (out, (self.n, 3))):
+                if not (isinstance(a, t.Tensor) and a.is_cuda and tuple(a.shape) == shape and
+                        a.dtype == t.float64 and a.is_contiguous() and
+                        a.device.index == self.device_index):
+                    raise ParameterError("derivative expects contiguous float64 CUDA tensors "
+                                         f"m (n, 3), u (n_in,), out (n, 3) on {self._dev}")
             self._plan.derivative_dev(m, u, out)
             return out
         m_d = t.as_tensor(np.ascontiguousarray(m, dtype=np.float64)).to(self._dev)
@@ -112,6 +118,12 @@ class B200Backend:
         IntegrationDivergedError(oscillator, step) like `integrator.py:174-177`.
         """
         t = self._torch
+        samples = np.asarray(samples, dtype=np.float64)
+        if np.shape(m0) != (self.n, 3):
+            raise ParameterError(f"m0 must be ({self.n}, 3), got {np.shape(m0)}")
+        if samples.ndim != 2 or samples.shape[1] != self.n_in or samples.shape[0] < 1:
+            raise ParameterError(f"drive samples must be (n_samples, {self.n_in}), "
+                                 f"got {samples.shape}")
         nrec = _native.n_records(steps, stride)
         with t.cuda.device(self._dev):
             m_d = t.as_tensor(np.ascontiguousarray(m0, dtype=np.float64)).to(self._dev)
@@ -145,6 +157,8 @@ class B200Backend:
         per_member = samples.ndim == 3
         if per_member and samples.shape[0] != batch:
             raise ParameterError("per-member drive must be (B, n_samples, n_in)")
+        if samples.ndim not in (2, 3) or samples.shape[-1] != self.n_in or samples.shape[-2] < 1:
+            raise ParameterError(f"drive samples must be ([B,] n_samples, {self.n_in})")
         stride_m = samples.shape[1] * samples.shape[2] if per_member else 0
         nrec = _native.n_records(steps, stride)
         with t.cuda.device(self._dev):

@@ -264,6 +264,13 @@ size_t grid_smem(int rows_cap, const ColSched &cs, int chunk_cols, bool resident
 }
 
 int choose_chunk(const ColSched &cs, int rows_cap, bool resident) {
+    // STO_CHUNK_COLS (tests): force x windows of that many physical columns
+    // (rounded down to whole blocks) even when the row fits one window, so the
+    // chunked block loop that N >~ 2.4e4 takes is exercised at small N.
+    if (const char *e = getenv("STO_CHUNK_COLS")) {
+        const int c = atoi(e) / cs.blk * cs.blk;
+        if (c >= cs.blk && c < cs.ldw && grid_smem(rows_cap, cs, c, resident) <= kSmemBudget) return c;
+    }
     if (grid_smem(rows_cap, cs, cs.ldw, resident) <= kSmemBudget) return cs.ldw;
     int chunk = 16384;
     while (chunk > cs.blk && grid_smem(rows_cap, cs, chunk, resident) > kSmemBudget) chunk >>= 1;
@@ -757,7 +764,8 @@ int sto_plan_get_info(const sto_plan *P, sto_plan_info *info) {
     info->smem_bytes = (int)P->smem;
     info->ldw = P->L.cs.ldw;
     info->block_cols = P->L.cs.blk;
-    info->w_bytes = (int64_t)P->n * P->L.cs.ldw * (int64_t)sizeof(double);
+    info->w_bytes = (int64_t)P->rows * P->L.cs.ldw * (int64_t)sizeof(double);
+    info->x_window_cols = (P->kind == kStream || P->kind == kResident) ? P->chunk_cols : P->L.cs.ldw;
     return STO_OK;
 }
 
@@ -830,7 +838,9 @@ int sto_integrate(sto_plan *P, const sto_run *r, sto_status *status, void *strea
     switch (P->kind) {
         case kTiny: rc = launch_tiny(p, P->n, s); break;
         case kReg: {
-            RegParams rp{p, P->ll};
+            RegParams rp{p, P->ll, 0u};
+            // test knob: start the 31-bit LL epoch near its wrap (STO_REG_EPOCH0, even)
+            if (const char *e = getenv("STO_REG_EPOCH0")) rp.epoch0 = (unsigned)strtoul(e, nullptr, 0) & 0x7ffffffeu;
             STO_CUDA(cudaMemsetAsync(P->ll, 0, sizeof(uint4) * 2 * (size_t)P->n, s));
             rc = launch_reg(rp, P->team, P->rows_per_team, P->chunk_cols == 1, P->grid, P->threads,
                             P->smem, s);

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
             const bool record = (step == next_rec) || (step == p.steps);
 #pragma unroll
             for (int stage = 0; stage < 4; ++stage) {
-                const long long estage = (step - 1) * 4 + stage;
+                [[maybe_unused]] const long long estage = (step - 1) * 4 + stage;
                 const int buf = stage & 1;  // compile-time after unrolling
                 if (!(step == 1 && stage == 0)) {
                     // phases of buffer 1: stages 1, 3 -> parity 0, 1; buffer 0: stages 2, 0 -> 0, 1
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
         }
     } else {
         // ==================== owners: RHS, RK4 update, publication ==========
-        const int lane = threadIdx.x;
+        [[maybe_unused]] const int lane = threadIdx.x;
         auto u_of = [&](long long st) {  // drive sample of step `st` (zero-order hold, model.py:93-149)
             return p.n_samples > 1 ? p.samples + ((st - 1) / p.sps) * p.n_in : p.samples;
         };
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
             const bool record = (step == next_rec) || (step == p.steps);
 #pragma unroll
             for (int stage = 0; stage < 4; ++stage) {
-                const long long estage = (step - 1) * 4 + stage;
+                [[maybe_unused]] const long long estage = (step - 1) * 4 + stage;
                 // row sums in cps.  `pre` is tied to the barrier so the compiler cannot
                 // sink the own-state half (IEEE division included) past it: it must
                 // run while the GEMV warps work, not after the row sums arrive
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
             const bool record = (step == next_rec) || (step == p.steps);
 #pragma unroll
             for (int stage = 0; stage < 4; ++stage) {
-                const long long estage = (step - 1) * 4 + stage;
+                [[maybe_unused]] const long long estage = (step - 1) * 4 + stage;
                 const int buf = stage & 1;
                 if (!(step == 1 && stage == 0)) {
                     clu_wait(buf ? bar1 : bar0, (stage == 1 || stage == 2) ? 0u : 1u);

@@ -34,6 +34,7 @@ namespace sto {
 struct RegParams {
     KParams k;              // shared fields (consts, run, states, status ...)
     uint4 *ll;              // [2][n] LL words of the published x (zeroed before launch)
+    unsigned epoch0;        // first exchange epoch - 1 (0; STO_REG_EPOCH0 tests the wrap)
 };
 
 constexpr int kLLMaxPerThread = 4;  // n <= 4 * 512
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __
 
     long long next_rec = p.stride;
     long long rec_idx = 1;
-    unsigned epoch = 0;
+    unsigned epoch = rp.epoch0;
     bool stop = false;
     RhsPre pre{};
     // input field of step `st` (zero-order hold, model.py:93-149)
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __
         const bool record = (step == next_rec) || (step == p.steps);
 #pragma unroll
         for (int stage = 0; stage < 4; ++stage) {  // unrolled: per-stage branches resolve at compile time
-            const long long estage = (step - 1) * 4 + stage;
+            [[maybe_unused]] const long long estage = (step - 1) * 4 + stage;
             TL(estage, 0);
             // -------- team GEMV: pinned tree of w . x ----------------------
             // products streamed pair by pair through an unrolled binary
@@ -232,7 +233,11 @@ __global__ void __launch_bounds__(R == 2 ? 256 : 512, 1) reg_rk4_kernel(const __
                 TL(estage, 3);
                 if (*sstop) stop = true;
             } else {
-                ++epoch;
+                // 31-bit epochs (bit 31 is the stop bit): after 0x7fffffff the
+                // count restarts at 2, keeping the buffer parity alternating and
+                // never matching a zeroed (unwritten) word; a slot is rewritten
+                // every 2 stages, so a stale word can only hold epoch - 2
+                if (++epoch == 0x80000000u) epoch = 2u;
                 if (owner)
                     st_ll(rp.ll + (size_t)(epoch & 1) * n + k, xpub, epoch | (bad ? 0x80000000u : 0u));
                 TL(estage, 2);

@@ -58,13 +58,18 @@ def _whole_run_integrate(original):
     import spinosc.integrator as ref
 
     def integrate(topology, params, config, backend=None):
-        if backend is None and topology.n == config.n:
+        if topology.n != config.n:  # the reference's checks come first (integrator.py:139-150)
+            return original(topology, params, config, backend=backend)
+        if backend is None:
             from spinosc.backends import create_backend
 
             backend = create_backend(config.backend, topology, params, workers=config.workers,
                                      gpu_device=config.gpu_device)
-        if backend is None or not hasattr(backend, "integrate_run"):
+        if not hasattr(backend, "integrate_run"):
             return original(topology, params, config, backend=backend)
+        if getattr(backend, "n", config.n) != config.n:
+            raise ref.ParameterError(
+                f"backend is for {backend.n} oscillators, config.n is {config.n}")
         series = config.input_series
         if series is None:
             series = ref.InputSeries.zeros(topology.n_in)

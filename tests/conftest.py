@@ -68,3 +68,22 @@ def spinosc_ref():
         sys.path.append(str(ref))
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_sto")
     return pytest.importorskip("spinosc")
+
+
+def horizon_topology(d: dict):
+    """build_topology(n, seed) for a full-horizon fixture (hz_*.npz, which stores
+    only W's sha256): rebuilt here, and refused unless its bits are the
+    reference's (W depends on the LAPACK build behind the spectral radius)."""
+    import hashlib
+
+    from paper_2312_01121_b200 import build_topology
+
+    top = build_topology(int(d["n"]), n_in=1, seed=int(d["seed"]))
+    w = np.ascontiguousarray(top.coupling.entries)
+    w_in = np.ascontiguousarray(top.input_weights.entries)
+    assert hashlib.sha256(w.tobytes()).hexdigest() == str(d["w_sha256"]), "W bits differ"
+    assert hashlib.sha256(w_in.tobytes()).hexdigest() == str(d["w_in_sha256"]), "W_in differs"
+    return top
+
+
+HORIZONS = ["hz_n1_1e6.npz", "hz_n1000_1e5.npz"]

@@ -149,8 +149,40 @@ def make_trajs(tops: dict) -> None:
     run_case("n6_diverge_late", late, p, 100, 1e-11, 10, InputSeries(drive, 5))
 
 
+def make_horizons() -> None:
+    """BASELINE configs[1] and configs[2] at their FULL horizons, by the
+    reference's own numba engines (bit-identical to "reference", A2):
+      hz_n1_1e6.npz      N = 1, u = 0, 1e6 RK4 steps, recorded every 1e5
+      hz_n1000_1e5.npz   N = 1000, build_topology(1000, seed=0), u = 0, 1e5
+                         steps, recorded every 1e4
+    W is not stored (8 MB): the consumer rebuilds build_topology(1000, seed=0)
+    and must first match `w_sha256` / `w_in_sha256` (W's bits depend on the
+    LAPACK build of the spectral radius)."""
+    import hashlib
+
+    p = PhysicalParams()
+    for name, n, steps, stride, engine in (("hz_n1_1e6", 1, 1_000_000, 100_000, "fused"),
+                                           ("hz_n1000_1e5", 1000, 100_000, 10_000, "parallel")):
+        top = build_topology(n, n_in=1, seed=0)
+        cfg = RunConfig(n=n, steps=steps, dt=1e-11, record_stride=stride, backend=engine)
+        traj = integrate(top, p, cfg)
+        w = np.ascontiguousarray(top.coupling.entries)
+        w_in = np.ascontiguousarray(top.input_weights.entries)
+        np.savez(OUT / f"{name}.npz", n=n, seed=0, steps=steps, stride=stride, dt=1e-11,
+                 consts=np.array(_scalar_pack(p)), m0=initial_state(n),
+                 w_sha256=hashlib.sha256(w.tobytes()).hexdigest(),
+                 w_in_sha256=hashlib.sha256(w_in.tobytes()).hexdigest(),
+                 states=traj.states, times=traj.times, drift=traj.max_norm_drift,
+                 engine=engine)
+        print(name, f"drift={traj.max_norm_drift:.3e}", f"{traj.elapsed_seconds:.1f}s")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["horizons"]:
+        make_horizons()
+        sys.exit(0)
     make_tree()
     tops = make_topos()
     make_deriv(tops)
     make_trajs(tops)
+    make_horizons()

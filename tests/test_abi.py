@@ -50,7 +50,7 @@ def test_library_exports_every_declared_symbol(native):
 
 def test_calls_that_need_no_gpu(native):
     lib = native.lib()
-    assert lib.sto_abi_version() == 1
+    assert lib.sto_abi_version() == 2
     assert lib.sto_n_records(10, 3) == 5
     assert lib.sto_n_records(10, 5) == 3
     assert lib.sto_n_records(0, 1) == 0

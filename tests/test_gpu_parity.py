@@ -229,3 +229,127 @@ def test_streaming_warp_counts_bit_exact(sto, oracle_mod, monkeypatch, warps):
     assert info["kernel_name"] == "stream"
     assert info["threads"] == (512 if warps == "16" else 640), info
     assert_bit_equal(states, want, f"n=5000 warps={warps}")
+
+
+def _random_case(sto, n, seed, steps, stride, n_in=1, sps=1, scale=None):
+    g = np.random.default_rng(seed)
+    w = g.random((n, n))
+    w *= 2.0
+    w -= 1.0
+    w *= 1.0 / np.sqrt(n / 3.0) if scale is None else scale
+    np.fill_diagonal(w, 0.0)
+    w_in = g.uniform(-1, 1, (n, n_in))
+    samples = g.uniform(-1, 1, (-(-steps // sps), n_in))
+    return dict(w=w, w_in=w_in, consts=np.array(sto.kernel_scalars(sto.PhysicalParams())),
+                m0=sto.initial_state(n), samples=samples, steps_per_sample=sps, dt=1e-11,
+                steps=steps, stride=stride)
+
+
+@pytest.mark.parametrize("n,chunk", [(3000, 1024), (5000, 512), (5000, 1024), (5000, 2048),
+                                     (9000, 2048), (9000, 4096)])
+def test_chunked_x_windows_bit_exact(sto, oracle_mod, monkeypatch, n, chunk):
+    """The streaming kernel's chunked block loop (x staged in several shared-memory
+    windows: per-chunk staging, bfirst / bcount, x_base offsets) -- the path every
+    N >~ 2.4e4 run takes -- forced at small N with STO_CHUNK_COLS: bit-exact vs the
+    oracle for the L2 (N = 3000) and HBM-streaming (N >= 5000) variants, whole
+    run and a single derivative (K0)."""
+    monkeypatch.setenv("STO_CHUNK_COLS", str(chunk))
+    d = _random_case(sto, n, 7 * n + chunk, steps=5, stride=2, n_in=2, sps=2)
+    want, _ = oracle_mod.integrate(d["w"], d["w_in"], d["consts"], d["m0"], d["samples"], 2,
+                                   1e-11, 5, 2)
+    states, final, info = _run(sto, d, "stream")
+    assert info["kernel_name"] == "stream"
+    assert info["x_window_cols"] == chunk and -(-info["ldw"] // chunk) >= 2, info
+    assert_bit_equal(states, want, f"n={n} chunk={chunk}")
+    assert_bit_equal(final, want[-1], "final")
+
+    from paper_2312_01121_b200.backends.b200 import B200Backend
+
+    top = _topology(sto, d)
+    be = B200Backend(top, None, device=0, consts=d["consts"])
+    m = np.random.default_rng(n).standard_normal((n, 3))
+    u = np.array([0.3, -0.7])
+    out = np.empty((n, 3))
+    be.derivative(m, u, out)
+    assert_bit_equal(out, oracle_mod.derivative(d["w"], d["w_in"], d["consts"], m, u,
+                                                threads=oracle_mod.default_threads()),
+                     f"derivative n={n} chunk={chunk}")
+
+
+def test_n3e4_chunked_streaming_against_oracle(sto, oracle_mod):
+    """N = 3e4 (W 7.2 GB): the real chunked-x configuration of configs[4]'s upper
+    half (x = 2 windows of 16384 columns, chosen by the host, no knob), 2 RK4
+    steps, bit-exact vs the oracle."""
+    n = 30_000
+    d = _random_case(sto, n, 30, steps=2, stride=1)
+    d["samples"] = np.zeros((1, 1))
+    want, _ = oracle_mod.integrate(d["w"], d["w_in"], d["consts"], d["m0"], d["samples"], 1,
+                                   1e-11, 2, 1)
+    states, final, info = _run(sto, d, "auto")
+    assert info["kernel_name"] == "stream"
+    assert info["x_window_cols"] < info["ldw"], info
+    assert_bit_equal(states, want, "n=3e4")
+    assert_bit_equal(final, want[-1], "n=3e4 final")
+
+
+def test_register_kernel_epoch_wrap(sto, oracle_mod, monkeypatch):
+    """The register kernel's LL exchange counts 31-bit epochs (bit 31 is the stop
+    bit); runs longer than 2^29 RK4 steps wrap it.  STO_REG_EPOCH0 starts the
+    count 16 stages before the wrap: the run must stay bit-exact (a counter that
+    reached bit 31 would never match again and hang the kernel)."""
+    monkeypatch.setenv("STO_REG_EPOCH0", str(0x7FFFFFF0))
+    d = _random_case(sto, 1000, 1000, steps=30, stride=7)
+    want, _ = oracle_mod.integrate(d["w"], d["w_in"], d["consts"], d["m0"], d["samples"], 1,
+                                   1e-11, 30, 7)
+    states, _, info = _run(sto, d, "reg")
+    assert info["kernel_name"] == "reg"
+    assert_bit_equal(states, want, "epoch wrap")
+
+
+@pytest.mark.parametrize("n,split,sps,stride", [(100, 500, 1, 100), (100, 501, 3, 167),
+                                               (1000, 60, 4, 20), (3000, 7, 2, 7)])
+def test_resume_on_device_bit_exact(sto, oracle_mod, n, split, sps, stride):
+    """f4 on the B200 path: run(a + b) == run(a) + resume(b) bit for bit (split
+    inside a drive hold for 501 % 3), through the cluster / register /
+    streaming kernels, and equal to the oracle."""
+    total = 2 * split + (3 if split % 2 else 0)
+    top = sto.build_topology(n, seed=n + split)
+    p = sto.PhysicalParams()
+    g = np.random.default_rng(split)
+    full = sto.InputSeries(g.uniform(-1, 1, (-(-total // sps), 1)), sps)
+    head = sto.InputSeries(full.samples[:-(-split // sps)], sps)
+    whole = sto.integrate(top, p, sto.RunConfig(n=n, steps=total, dt=1e-11, record_stride=stride,
+                                                input_series=full))
+    first = sto.integrate(top, p, sto.RunConfig(n=n, steps=split, dt=1e-11, record_stride=stride,
+                                                input_series=head))
+    rest = sto.resume(first, top, p, total - split, input_series=full)
+    assert_bit_equal(np.concatenate([first.states, rest.states[1:]]), whole.states, "resume")
+    assert np.array_equal(np.concatenate([first.times, rest.times[1:]]), whole.times)
+    want, _ = oracle_mod.integrate(top.coupling.entries, top.input_weights.entries,
+                                   sto.kernel_scalars(p), sto.initial_state(n), full.samples, sps,
+                                   1e-11, total, stride)
+    assert_bit_equal(whole.states, want, "whole vs oracle")
+
+
+@pytest.mark.parametrize("name,families", [("hz_n1_1e6.npz", ["auto", "single"]),
+                                           ("hz_n1000_1e5.npz", ["auto", "stream"])])
+def test_full_horizon_configs(sto, name, families):
+    """configs[1] (N = 1, 1e6 RK4 steps) and configs[2] (N = 1000,
+    build_topology(1000, seed=0), 1e5 steps) at the horizons BASELINE names,
+    bit-exact against the reference's own trajectories (fixtures made by its
+    numba engines), through the public integrate() and a second kernel family."""
+    from conftest import horizon_topology
+
+    d = load_golden(name)
+    top = horizon_topology(d)
+    n, steps, stride = int(d["n"]), int(d["steps"]), int(d["stride"])
+    cfg = sto.RunConfig(n=n, steps=steps, dt=float(d["dt"]), record_stride=stride)
+    traj = sto.integrate(top, sto.PhysicalParams(), cfg)
+    assert_bit_equal(traj.states, d["states"], f"{name} public integrate")
+    assert traj.max_norm_drift == float(d["drift"])
+    dd = dict(w=top.coupling.entries, w_in=top.input_weights.entries, consts=d["consts"],
+              m0=d["m0"], samples=np.zeros((1, 1)), steps_per_sample=1, dt=float(d["dt"]),
+              steps=steps, stride=stride)
+    for fam in families[1:]:
+        states, _, info = _run(sto, dd, fam)
+        assert_bit_equal(states, d["states"], f"{name} [{fam}: {info['kernel_name']}]")

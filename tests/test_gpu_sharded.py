@@ -14,11 +14,18 @@ from conftest import assert_bit_equal
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,world,fam", [(1000, 2, 0), (1000, 3, 0x1), (3001, 4, 0x1),
-                                         (10000, 2, 0), (257, 8, 0)])
-def test_logical_ranks_bit_exact(oracle_mod, n, world, fam):
+@pytest.mark.parametrize("n,world,fam,chunk", [(1000, 2, 0, 0), (1000, 3, 0x1, 0), (3001, 4, 0x1, 0),
+                                               (10000, 2, 0, 0), (257, 8, 0, 0),
+                                               (5000, 2, 0x1, 2048), (5000, 4, 0x1, 1024),
+                                               (3001, 3, 0x1, 512)])
+def test_logical_ranks_bit_exact(oracle_mod, monkeypatch, n, world, fam, chunk):
+    """chunk > 0: every rank's streaming kernel stages x in windows of `chunk`
+    columns (STO_CHUNK_COLS), the chunked MULTI path."""
     import paper_2312_01121_b200 as sto
     from paper_2312_01121_b200.sharding import integrate_logical
+
+    if chunk:
+        monkeypatch.setenv("STO_CHUNK_COLS", str(chunk))
 
     g = np.random.default_rng(n + world)
     w = g.uniform(-1, 1, (n, n)) / np.sqrt(n / 3.0)

@@ -327,3 +327,90 @@ def test_write_trajectory_csv_public_api(tmp_path):
                           config=sto.RunConfig(n=5, steps=20, dt=1e-11), elapsed_seconds=0.0)
     sto.write_trajectory_csv(tmp_path / "a.csv", traj)
     assert (tmp_path / "a.csv").read_text() == _reference_csv_text(traj.times, states)
+
+
+class _OracleDerivative:
+    """Derivative-only test double (the pinned C oracle): steps through the
+    stagewise path of integrate()."""
+
+    def __init__(self, top, params):
+        from oracle import oracle
+
+        import paper_2312_01121_b200 as sto
+
+        self._o, self._top = oracle, top
+        self._c = sto.kernel_scalars(params)
+
+    def derivative(self, m, u, out):
+        out[...] = self._o.derivative(self._top.coupling.entries, self._top.input_weights.entries,
+                                      self._c, m, u)
+        return out
+
+
+@pytest.mark.parametrize("split,sps,stride", [(60, 3, 20), (61, 3, 61), (45, 1, 15)])
+def test_resume_continues_bit_exact(params, oracle_mod, split, sps, stride):
+    """f4: run(a + b) == run(a) + resume(b), bit for bit -- also when the split
+    falls inside a held drive sample (61 % 3 != 0); and both equal the oracle."""
+    import paper_2312_01121_b200 as sto
+
+    n, total = 24, 120
+    top = sto.build_topology(n, seed=9)
+    g = np.random.default_rng(split)
+    full = sto.InputSeries(g.uniform(-1, 1, (-(-total // sps), 1)), sps)
+    head = sto.InputSeries(full.samples[:-(-split // sps)], sps)
+    be = _OracleDerivative(top, params)
+    whole = sto.integrate(top, params, sto.RunConfig(n=n, steps=total, dt=1e-11,
+                                                     record_stride=stride, input_series=full),
+                          backend=be)
+    first = sto.integrate(top, params, sto.RunConfig(n=n, steps=split, dt=1e-11,
+                                                     record_stride=stride, input_series=head),
+                          backend=be)
+    rest = sto.resume(first, top, params, total - split, backend=be, input_series=full)
+    assert rest.step_offset == split
+    got = np.concatenate([first.states, rest.states[1:]])
+    times = np.concatenate([first.times, rest.times[1:]])
+    assert np.array_equal(times, whole.times)
+    assert np.array_equal(got.view(np.uint64), whole.states.view(np.uint64))
+    want, _ = oracle_mod.integrate(top.coupling.entries, top.input_weights.entries,
+                                   sto.kernel_scalars(params), sto.initial_state(n), full.samples,
+                                   sps, 1e-11, total, stride)
+    assert np.array_equal(whole.states.view(np.uint64), want.view(np.uint64))
+
+
+def test_integrate_custom_m0_and_checks(params):
+    import paper_2312_01121_b200 as sto
+
+    n = 5
+    top = sto.build_topology(n, seed=2)
+    be = _OracleDerivative(top, params)
+    m0 = np.random.default_rng(0).standard_normal((n, 3))
+    m0 /= np.linalg.norm(m0, axis=1, keepdims=True)
+    keep = m0.copy()
+    traj = sto.integrate(top, params, sto.RunConfig(n=n, steps=10, dt=1e-11), backend=be, m0=m0)
+    assert np.array_equal(traj.states[0], keep) and np.array_equal(m0, keep)  # m0 untouched
+    with pytest.raises(sto.ParameterError):
+        sto.integrate(top, params, sto.RunConfig(n=n, steps=10, dt=1e-11), backend=be,
+                      m0=np.zeros((n + 1, 3)))
+    with pytest.raises(sto.ParameterError):
+        sto.integrate(top, params, sto.RunConfig(n=n, steps=10, dt=1e-11), backend=be,
+                      step_offset=-1)
+
+
+def test_resume_divergence_reports_global_step(params):
+    import paper_2312_01121_b200 as sto
+
+    def poison(m, u, out):
+        out[...] = 0.0
+        if u[0] > 0.5:
+            out[2, 0] = np.inf
+
+    top = sto.Topology.decoupled(4)
+    drive = np.zeros((40, 1))
+    drive[25:] = 1.0
+    series = sto.InputSeries(drive, 1)
+    first = sto.integrate(top, params, sto.RunConfig(
+        n=4, steps=20, dt=1e-11, record_stride=5, input_series=sto.InputSeries(drive[:20], 1)),
+        backend=_Stub(poison))
+    with pytest.raises(sto.IntegrationDivergedError) as info:
+        sto.resume(first, top, params, 20, backend=_Stub(poison), input_series=series)
+    assert (info.value.oscillator, info.value.step) == (2, 30)

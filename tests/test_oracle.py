@@ -67,3 +67,18 @@ def test_signed_zero_carry(oracle_mod):
     assert np.signbit(oracle_mod.tree_sum([-0.0]))
     assert np.signbit(oracle_mod.tree_sum([-0.0, -0.0, -0.0]))
     assert not np.signbit(oracle_mod.tree_sum([-0.0, 0.0, -0.0]))
+
+
+@pytest.mark.parametrize("name", ["hz_n1_1e6.npz", "hz_n1000_1e5.npz"])
+def test_full_horizon_fixtures(oracle_mod, name):
+    """BASELINE configs[1] (N = 1, 1e6 steps) and configs[2] (N = 1000, seed-0
+    W, 1e5 steps) at their full horizons, as the reference's own numba engines
+    produced them: the oracle must reproduce every recorded state."""
+    from conftest import horizon_topology
+
+    d = load_golden(name)
+    top = horizon_topology(d)
+    states, final = oracle_mod.integrate(top.coupling.entries, top.input_weights.entries,
+                                         d["consts"], d["m0"], np.zeros((1, 1)), 1,
+                                         float(d["dt"]), int(d["steps"]), int(d["stride"]))
+    assert_bit_equal(states, d["states"], name)
