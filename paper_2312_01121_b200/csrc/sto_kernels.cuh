@@ -158,12 +158,23 @@ __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInf
     }
     if (threadIdx.x < mp.world) {
         unsigned long long f, t0 = 0;
+        bool stop = false;
         for (unsigned it = 0;; ++it) {
             asm volatile("ld.relaxed.sys.global.u64 %0, [%1];"
                          : "=l"(f)
                          : "l"(sh.flags + (size_t)threadIdx.x * kFlagSlot)
                          : "memory");
-            if ((f & ~(1ull << 63)) >= epoch) break;
+            const unsigned long long fe = f & ~(1ull << 63);
+            if (fe >= epoch) {
+                // A peer may already be ONE epoch ahead (it passed this exchange
+                // and raised the next flag before we polled).  Its stop bit then
+                // belongs to that next exchange: honour it only on the epoch it
+                // was raised for, so that every rank stops after the same
+                // exchange (else this rank would stop one exchange early and the
+                // peer would wait for our next flag forever).
+                stop = (f >> 63) && fe == epoch;
+                break;
+            }
             // watchdog: a peer that never arrives (its process died or never
             // launched) must not hang this GPU -- report it and stop
             if ((it & 1023u) == 1023u) {
@@ -171,13 +182,13 @@ __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInf
                 if (t0 == 0) t0 = t;
                 else if (t - t0 > mp.timeout_ns) {
                     report_peer_timeout(const_cast<StatusDev *>(status), threadIdx.x);
-                    f = 1ull << 63;
+                    stop = true;
                     break;
                 }
             }
         }
         asm volatile("fence.acq_rel.sys;" ::: "memory");
-        if (f >> 63) *sflag = 1;
+        if (stop) *sflag = 1;
     }
     __syncthreads();
     return *sflag != 0;

@@ -25,7 +25,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
-from .errors import ParameterError
+from .errors import IntegrationDivergedError, ParameterError, SpinoscError
 from .params import kernel_scalars
 
 
@@ -84,6 +84,86 @@ def integrate_logical(topology, params, m0: np.ndarray, samples: np.ndarray,
             p.close()
 
 
+# status words agreed across ranks after every sharded run (agree_status)
+RUN_OK, RUN_DIVERGED, RUN_FAILED = 0, 1, 2
+
+
+def collective_device(group=None):
+    """Device of the tensors a collective on `group` takes: the current CUDA
+    device under NCCL, the host under gloo (CPU tests, STO_BENCH_SHARE_GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def agree_status(status: tuple[int, int, int], group=None,
+                 local_error: Exception | None = None) -> None:
+    """Every rank raises the same error after a sharded run, or none does.
+
+    `status` = (RUN_*, oscillator, step) of this rank's launch.  A divergence
+    is detected by the rank owning the bad row only; its peers learn of it
+    through the divergence bit of that epoch's exchange flag and stop cleanly
+    at the same epoch with an OK status.  Without this exchange the owning
+    rank would raise while its peers went on into the state gather and
+    blocked forever.  The earliest (step, oscillator) over the diverged ranks
+    is the reference's report (integrator.py:174-177: first bad recorded step,
+    first bad row in it); a watchdog stop or CUDA error on any rank becomes a
+    SpinoscError on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    mine = torch.tensor([int(v) for v in status], dtype=torch.int64,
+                        device=collective_device(group))
+    every = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(every, mine, group=group)
+    rows = [tuple(int(v) for v in t.cpu().tolist()) for t in every]
+    failed = [r for r, s in enumerate(rows) if s[0] == RUN_FAILED]
+    if failed:
+        why = f": {local_error}" if local_error is not None else "; see that rank's error"
+        raise SpinoscError(f"sharded run failed on rank(s) {failed} (peer watchdog or CUDA "
+                           f"error){why}") from local_error
+    bad = [(s[2], s[1]) for s in rows if s[0] == RUN_DIVERGED]
+    if bad:
+        step, osc = min(bad)
+        raise IntegrationDivergedError(oscillator=osc, step=step)
+
+
+def gather_rows(block, shards: list[tuple[int, int]], n: int, group=None):
+    """All-gather row blocks into the full array on every rank.
+
+    `block` is this rank's (R, rows_r, 3) slice of a row-sharded array (a
+    torch tensor on `collective_device(group)`); returns the (R, n, 3) tensor
+    with every rank's rows in place.  Device-side under NCCL: one padded
+    all_gather over NVLink instead of pickling every rank's states."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rows_max = max(c for _, c in shards)
+    rank = dist.get_rank(group)
+    if block.shape[1] != shards[rank][1]:
+        raise ParameterError("row block does not match this rank's shard")
+    padded = torch.zeros((block.shape[0], rows_max, *block.shape[2:]), dtype=block.dtype,
+                         device=block.device)
+    padded[:, :block.shape[1]] = block
+    parts = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(parts, padded, group=group)
+    return torch.cat([parts[r][:, :c] for r, (_, c) in enumerate(shards)], dim=1)
+
+
+def shard_members(batch: int, world: int, rank: int) -> np.ndarray:
+    """Member indices rank `rank` integrates when a batch of independent
+    ensemble members is batch-sharded over `world` ranks (contiguous and
+    balanced, so the gathered order is the member order)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ParameterError(f"bad rank {rank} of {world}")
+    return np.array_split(np.arange(batch), world)[rank]
+
+
 class ShardedB200Backend:
     """One rank of a row-sharded trajectory (one process per GPU, torch.distributed).
 
@@ -114,23 +194,33 @@ class ShardedB200Backend:
 
     def integrate_run(self, m0: np.ndarray, samples: np.ndarray, steps_per_sample: int,
                       dt: float, steps: int, stride: int) -> np.ndarray:
+        """The whole run on every rank; returns the full recorded grid (R, n, 3)
+        on every rank and updates m0 (n, 3) in place.  A divergence raises
+        IntegrationDivergedError on every rank (agree_status)."""
         torch, dist = self._torch, self._dist
         dev = torch.device("cuda", self.device)
         begin, count = self.shards[self.rank]
         m_d = torch.as_tensor(np.ascontiguousarray(m0, dtype=np.float64)).to(dev)
         s_d = torch.as_tensor(np.ascontiguousarray(samples, dtype=np.float64)).to(dev)
         nrec = _native.n_records(steps, stride)
-        states = torch.zeros((nrec, self.n, 3), dtype=torch.float64, device=dev)
+        states = torch.zeros((nrec + 1, self.n, 3), dtype=torch.float64, device=dev)
         dist.barrier(group=self._group)  # nobody starts before every peer finished the last run
-        self._plan.integrate_dev(m_d, s_d, steps_per_sample, dt, steps, stride, states, sync=True)
-        mine = states[:, begin:begin + count].cpu().numpy()
-        blocks: list = [None] * self.world
-        dist.all_gather_object(blocks, (mine, m_d[begin:begin + count].cpu().numpy()),
-                               group=self._group)
-        full = assemble_states([b[0] for b in blocks], self.shards, self.n)
-        for (b, c), blk in zip(self.shards, blocks):
-            m0[b:b + c] = blk[1]
-        return full
+        local_error = None
+        try:
+            self._plan.integrate_dev(m_d, s_d, steps_per_sample, dt, steps, stride, states,
+                                     sync=True)
+            status = (RUN_OK, 0, 0)
+        except IntegrationDivergedError as exc:
+            status = (RUN_DIVERGED, exc.oscillator, exc.step)
+        except SpinoscError as exc:
+            status, local_error = (RUN_FAILED, 0, 0), exc
+        agree_status(status, self._group, local_error)
+        # final state rides along as one more "record" of this rank's rows
+        states[nrec, begin:begin + count] = m_d[begin:begin + count]
+        block = states[:, begin:begin + count].to(collective_device(self._group))
+        full = gather_rows(block, self.shards, self.n, self._group).cpu().numpy()
+        np.copyto(m0, full[nrec])
+        return full[:nrec]
 
     def close(self) -> None:
         self._plan.close()

@@ -72,18 +72,27 @@ def spinosc_ref():
 
 def horizon_topology(d: dict):
     """build_topology(n, seed) for a full-horizon fixture (hz_*.npz, which stores
-    only W's sha256): rebuilt here, and refused unless its bits are the
-    reference's (W depends on the LAPACK build behind the spectral radius)."""
+    only W's sha256 and the reference's rho): W = the seeded PCG64 draws / rho,
+    the reference's own steps (topology.py:241-265) with rho taken from the
+    fixture.  rho comes out of LAPACK (the Arnoldi eigensolve), whose bits
+    depend on the host's BLAS build and CPU, so the GPU box must not recompute
+    it; the draws and the elementwise IEEE division are portable.  The rebuilt
+    W is refused unless its bits are the ones the reference integrated."""
     import hashlib
 
-    from paper_2312_01121_b200 import build_topology
+    from paper_2312_01121_b200 import CouplingMatrix, InputWeights, Topology
+    from paper_2312_01121_b200.topology import RngStream
 
-    top = build_topology(int(d["n"]), n_in=1, seed=int(d["seed"]))
-    w = np.ascontiguousarray(top.coupling.entries)
-    w_in = np.ascontiguousarray(top.input_weights.entries)
+    n, rho = int(d["n"]), float(d["rho"])
+    stream = RngStream(int(d["seed"]))
+    w = np.zeros((n, n))
+    if n > 1:
+        w[~np.eye(n, dtype=bool)] = stream.uniform_pm1(n * (n - 1))
+        w /= rho
+    w_in = stream.uniform_pm1(n).reshape(n, 1)
     assert hashlib.sha256(w.tobytes()).hexdigest() == str(d["w_sha256"]), "W bits differ"
     assert hashlib.sha256(w_in.tobytes()).hexdigest() == str(d["w_in_sha256"]), "W_in differs"
-    return top
+    return Topology(CouplingMatrix(w), InputWeights(w_in))
 
 
 HORIZONS = ["hz_n1_1e6.npz", "hz_n1000_1e5.npz"]

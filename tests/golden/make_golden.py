@@ -149,15 +149,27 @@ def make_trajs(tops: dict) -> None:
     run_case("n6_diverge_late", late, p, 100, 1e-11, 10, InputSeries(drive, 5))
 
 
+def _reference_rho(n: int) -> float:
+    """The reference's rho for build_topology(n, seed=0) (topology.py:241-265)."""
+    from spinosc.topology import RngStream, spectral_radius
+
+    if n == 1:
+        return 0.0
+    w = np.zeros((n, n))
+    w[~np.eye(n, dtype=bool)] = RngStream(0).uniform_pm1(n * (n - 1))
+    return float(spectral_radius(w))
+
+
 def make_horizons() -> None:
     """BASELINE configs[1] and configs[2] at their FULL horizons, by the
     reference's own numba engines (bit-identical to "reference", A2):
       hz_n1_1e6.npz      N = 1, u = 0, 1e6 RK4 steps, recorded every 1e5
       hz_n1000_1e5.npz   N = 1000, build_topology(1000, seed=0), u = 0, 1e5
                          steps, recorded every 1e4
-    W is not stored (8 MB): the consumer rebuilds build_topology(1000, seed=0)
-    and must first match `w_sha256` / `w_in_sha256` (W's bits depend on the
-    LAPACK build of the spectral radius)."""
+    W is not stored (8 MB): the consumer rebuilds it from the seeded draws
+    divided by the stored `rho` and must first match `w_sha256` /
+    `w_in_sha256`.  rho is stored because its bits depend on the LAPACK build
+    and CPU behind the spectral radius; the GPU box's differs."""
     import hashlib
 
     p = PhysicalParams()
@@ -172,6 +184,7 @@ def make_horizons() -> None:
                  consts=np.array(_scalar_pack(p)), m0=initial_state(n),
                  w_sha256=hashlib.sha256(w.tobytes()).hexdigest(),
                  w_in_sha256=hashlib.sha256(w_in.tobytes()).hexdigest(),
+                 rho=_reference_rho(n),
                  states=traj.states, times=traj.times, drift=traj.max_norm_drift,
                  engine=engine)
         print(name, f"drift={traj.max_norm_drift:.3e}", f"{traj.elapsed_seconds:.1f}s")

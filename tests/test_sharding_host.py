@@ -15,7 +15,9 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2312_01121_b200.sharding import assemble_states, shard_rows
+from paper_2312_01121_b200.sharding import (RUN_DIVERGED, RUN_FAILED, RUN_OK, agree_status,
+                                            assemble_states, gather_rows, shard_members,
+                                            shard_rows)
 
 
 @pytest.mark.parametrize("n,world", [(8, 2), (10, 3), (10000, 8), (1001, 7)])
@@ -75,3 +77,67 @@ def test_gloo_world2_handle_exchange_and_assembly():
     results = sorted(q.get(timeout=10) for _ in procs)
     assert results == [(0, True), (1, True)]
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _collective_worker(rank, world, port, n, result_q):
+    """gather_rows (padded device-style all_gather of ragged row blocks) and
+    agree_status (every rank raises the same error) on a gloo group."""
+    import torch
+
+    from paper_2312_01121_b200 import IntegrationDivergedError, SpinoscError
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    try:
+        shards = shard_rows(n, world)
+        full = torch.arange(4 * n * 3, dtype=torch.float64).reshape(4, n, 3)
+        begin, count = shards[rank]
+        got = gather_rows(full[:, begin:begin + count].clone(), shards, n)
+        out["gather"] = bool(torch.equal(got, full))
+        agree_status((RUN_OK, 0, 0))  # nobody diverged: no error anywhere
+        out["ok"] = True
+        # ranks 1 and 2 diverge at different (step, oscillator): everyone reports the earliest
+        st = {1: (RUN_DIVERGED, 7, 40), 2: (RUN_DIVERGED, 3, 20)}.get(rank, (RUN_OK, 0, 0))
+        try:
+            agree_status(st)
+            out["div"] = None
+        except IntegrationDivergedError as e:
+            out["div"] = (e.oscillator, e.step)
+        # a watchdog stop on one rank fails every rank, even a diverged one
+        st = (RUN_FAILED, 0, 0) if rank == world - 1 else (RUN_DIVERGED, 1, 1)
+        try:
+            agree_status(st)
+            out["fail"] = None
+        except IntegrationDivergedError:
+            out["fail"] = "diverged"
+        except SpinoscError:
+            out["fail"] = "failed"
+        result_q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_status_agreement_and_row_gather():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_collective_worker, args=(r, world, port, 11, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    results = dict(q.get(timeout=10) for _ in procs)
+    assert all(p.exitcode == 0 for p in procs)
+    for r in range(world):
+        assert results[r] == {"gather": True, "ok": True, "div": (3, 20), "fail": "failed"}, results
+
+
+@pytest.mark.parametrize("batch,world", [(512, 8), (512, 3), (7, 4), (3, 3)])
+def test_shard_members_partition(batch, world):
+    got = np.concatenate([shard_members(batch, world, r) for r in range(world)])
+    assert np.array_equal(got, np.arange(batch))
+    sizes = [len(shard_members(batch, world, r)) for r in range(world)]
+    assert max(sizes) - min(sizes) <= 1

@@ -37,15 +37,36 @@ def main():
     m = sto.initial_state(n)
     states = be.integrate_run(m, series.samples, 1, 1e-11, steps, 1)
     states2 = be.integrate_run(sto.initial_state(n), series.samples, 1, 1e-11, steps, 1)  # epochs carry over
+    # a divergence on the LAST rank's rows: every rank must raise the same error
+    # (the peers stop on the flag's divergence bit and learn the report through
+    # agree_status) instead of the peers blocking in the state gather
+    bad = sto.initial_state(n)
+    bad[n - 2, 1] = np.nan
+    try:
+        be.integrate_run(bad, series.samples, 1, 1e-11, steps, 1)
+        div = None
+    except sto.IntegrationDivergedError as e:
+        div = (e.oscillator, e.step)
+    divs = [None] * dist.get_world_size()
+    dist.all_gather_object(divs, div)
+    states3 = be.integrate_run(sto.initial_state(n), series.samples, 1, 1e-11, steps, 1)  # still in step
     be.close()
     if dist.get_rank() == 0:
         from oracle import oracle
 
         want, _ = oracle.integrate(w, top.input_weights.entries, sto.kernel_scalars(params),
                                    sto.initial_state(n), series.samples, 1, 1e-11, steps, 1)
+        try:
+            oracle.integrate(w, top.input_weights.entries, sto.kernel_scalars(params), bad,
+                             series.samples, 1, 1e-11, steps, 1)
+            want_div = None
+        except oracle.OracleDiverged as e:
+            want_div = (e.oscillator, e.step)
         ok = bool(np.array_equal(states.view(np.uint64), want.view(np.uint64)) and
-                  np.array_equal(states2.view(np.uint64), want.view(np.uint64)))
-        print(json.dumps({"ok": ok, "world": dist.get_world_size(), "n": n, "steps": steps,
+                  np.array_equal(states2.view(np.uint64), want.view(np.uint64)) and
+                  np.array_equal(states3.view(np.uint64), want.view(np.uint64)) and
+                  all(d == want_div for d in divs))
+        print(json.dumps({"ok": ok, "world": dist.get_world_size(), "n": n, "steps": steps, "divergence_reports": divs,
                           "max_dev": float(np.abs(states - want).max())}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
