@@ -55,8 +55,15 @@ WORKLOADS = {
     "ens512": (1000, 10_000, "configs[3]: N=1000 x B=512 ensemble (current sweep 2.0-3.0 mA), "
                "1e4 RK4 steps, FP64 tensor-core (DMMA) coupling GEMM", False),
 }
+# dense recording (the reservoir-readout case, integrator.py:171-181): every
+# record_stride-th state is written to HBM in-kernel and read back in e2e
+WORKLOADS["n100_rec1"] = (100, 10_000, "configs[0] with record_stride=1: N=100, 1e4 RK4 steps, random "
+                          "drive, every state recorded (24 MB of states per run)", True)
+WORKLOADS["n1e4_rec10"] = (10_000, 1000, "configs[4] with record_stride=10: N=1e4, 1e3 RK4 steps, "
+                           "every 10th state recorded (24 MB of states per run)", False)
+RECORD_STRIDE = {"n100_rec1": 1, "n1e4_rec10": 10}
 ENSEMBLE_BATCH = {"ens512": 512}
-SHARDED_WORKLOADS = ("n1e4", "n4e4")  # row-sharded over GPUs when --gpus > 1
+SHARDED_WORKLOADS = ("n1e4", "n4e4", "n1e4_rec10")  # row-sharded over GPUs when --gpus > 1
 # FP64 peaks measured on this pool's B200 (tools/fp64_peak.cu; MEASURED_PEAKS.json has
 # none): DMMA m8n8k4 37.1 TFLOP/s, DFMA 34.0, cuBLAS DGEMM 8192^3 35.5.
 FP64_TENSOR_PEAK_TFLOPS = 37.1
@@ -291,8 +298,11 @@ def run_ours_ensemble(args, rank, world, local_rank):
         steps = args.rk4_steps
     batch_total = ENSEMBLE_BATCH[name]
     currents = np.linspace(2.0e-3, 3.0e-3, batch_total)
-    mine = np.array_split(np.arange(batch_total), world)[rank]   # batch sharding
-    params = [sto.PhysicalParams(current=float(c)) for c in currents[mine]]
+    from paper_2312_01121_b200.sharding import shard_members
+
+    mine = shard_members(batch_total, world, rank)   # batch sharding (no communication)
+    params_all = [sto.PhysicalParams(current=float(c)) for c in currents]
+    params = [params_all[i] for i in mine]
     top = cached_topology(n)
     backend = B200Backend(top, params[0], device=dev)
     consts = np.array([sto.kernel_scalars(p) for p in params])
@@ -334,13 +344,15 @@ def run_ours_ensemble(args, rank, world, local_rank):
     flops = 8.0 * n * n * batch * steps  # 4 stages x 2N MACs per oscillator-step
     achieved = flops / kernel_s / 1e12
 
-    # e2e through the public API, host buffers, each step
+    # e2e through the public API, host buffers, each step; with N ranks the
+    # batch-sharded integrate_ensemble(group=) returns every member on every rank
     cfg = sto.RunConfig(n=n, steps=steps, dt=DT, record_stride=stride, gpu_device=dev)
-    sto.integrate_ensemble(top, params, cfg, backend=backend)
+    group = "world" if dist else None
+    sto.integrate_ensemble(top, params_all, cfg, backend=backend, group=group)
     t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 2))
     for _ in range(e2e_steps):
-        ens = sto.integrate_ensemble(top, params, cfg, backend=backend)
+        ens = sto.integrate_ensemble(top, params_all, cfg, backend=backend, group=group)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if dist:
         t = torch.tensor([e2e_s], device="cuda")
@@ -370,7 +382,7 @@ def run_ours_ensemble(args, rank, world, local_rank):
                        "l2": "W 8 MB + stage x 8 MB L2-resident (fragment order), RK state in TMEM; one launch per run"},
             "e2e": {"value": batch_total * n * steps / e2e_s, "unit": "osc-steps/s",
                     "h2d_bytes_per_step": 8 * (n * n + n + batch * 3 * n + batch * 11),
-                    "d2h_bytes_per_step": 8 * ens.states.size},
+                    "d2h_bytes_per_step": 8 * ens.states.size // world},
             "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_TENSOR_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_TENSOR_PEAK_TFLOPS,
@@ -408,7 +420,7 @@ def run_ours(args, rank, world, local_rank):
     n, steps, desc, _ = WORKLOADS[name]
     if args.rk4_steps:
         steps = args.rk4_steps
-    stride = steps
+    stride = min(steps, RECORD_STRIDE.get(name, steps))
     params = sto.PhysicalParams()
     if world > 1 and rank != 0:
         dist.barrier()
@@ -592,6 +604,21 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def spawn_ranks(gpus: int) -> int:
+    """`python bench.py --gpus N` without torchrun: launch the N ranks (one
+    process per GPU) through torch.distributed.run on this node, exactly as
+    the driver's torchrun form would, and pass rank 0's JSON line through."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node",
+           str(gpus), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -602,7 +629,11 @@ def main():
     ap.add_argument("--rk4-steps", type=int, default=0, help="override RK4 steps per run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     rank, world, local_rank = env_rank()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
     elif args.workload in ENSEMBLE_BATCH:

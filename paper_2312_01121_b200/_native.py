@@ -17,7 +17,8 @@ import numpy as np
 from .errors import (BackendUnavailableError, IntegrationDivergedError, ParameterError,
                      SpinoscError)
 
-LIB_PATH = Path(__file__).resolve().parent / "libsto_b200.so"
+# STO_LIB: load another build of the same ABI from this directory (A/B timing of variants)
+LIB_PATH = Path(__file__).resolve().parent / os.environ.get("STO_LIB", "libsto_b200.so")
 
 STO_OK, STO_E_UNAVAILABLE, STO_E_PARAM, STO_E_DIVERGED, STO_E_CUDA, STO_E_NOMEM = range(6)
 

@@ -42,9 +42,15 @@
 // x = +0.0: in-register pinned tree + xor butterfly = the reference's padded
 // aligned tree, bit-exact.
 //
-// Divergence: on recording steps the owners check their state and every CTA
-// meets at one `barrier.cluster`, then reads all K "bad" flags through DSMEM,
-// so all CTAs stop after the same step (integrator.py:174-177).
+// Divergence (integrator.py:174-177): on a recording step every CTA sends,
+// with the step's last x publication, one 8-byte "bad" word to slot b of every
+// peer's flag array, counted on a third mbarrier (expect_tx(8 K) per recording
+// step).  The flags are off the critical path: stage 0 of the next step runs
+// on its x as usual, and at stage 1 -- whose x can only arrive long after the
+// flags left -- every CTA waits that mbarrier, reads the K words from its own
+// shared memory and takes the same stop decision (the extra stage is never
+// recorded).  No cluster barrier on the hot path (a barrier.cluster per
+// recording step cost ~2 k cycles: n100 at record_stride 1 ran +55 %).
 #pragma once
 
 #include "sto_reg_kernel.cuh"
@@ -52,6 +58,12 @@
 namespace sto {
 
 constexpr int kCluMaxK = 16;  // > 8: non-portable cluster size (B200 allows 16)
+// stop-flag rounds: at most one per kCluFlagEvery steps (every recording step
+// when the record stride is longer).  A row that diverges is reported in the
+// status at its own recording step either way (the earliest step wins,
+// report_divergence); the rounds only decide when the cluster stops, so a
+// diverged run computes at most kCluFlagEvery unrecorded extra steps.
+constexpr long long kCluFlagEvery = 64;
 
 __device__ __forceinline__ uint32_t clu_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -84,18 +96,21 @@ __device__ __forceinline__ void clu_bar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void clu_expect(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// Wait for a phase of a local mbarrier whose transactions are remote st.async
+// stores.  Poll with a RELAXED try_wait, then one acquire fence restricted to
+// shared::cluster: the data the peers' complete_tx released lands in this
+// CTA's shared memory, so no L1 invalidation is needed.  (An
+// `.acquire.cluster` try_wait makes ptxas put a CCTL.IVALL after EVERY poll,
+// which r1's hot-line profile showed as ~11 % of the N = 100 kernel's samples.)
 __device__ __forceinline__ void clu_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "CLU_WAIT_%=:\n\t"
-#ifdef STO_CLU_WAIT_CTA
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-#else
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-#endif
+        "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra CLU_WAIT_%=;\n}" ::"r"(bar),
         "r"(parity)
         : "memory");
+    asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
 }
 __device__ __forceinline__ void clu_sync() {  // every thread of every CTA of the cluster
     asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
@@ -123,7 +138,8 @@ __device__ __forceinline__ void clu_tl(long long e, int ev, bool me, double afte
 // shared-memory bytes of the cluster kernel for a padded row of P columns
 // (x double buffer, row sums, staging, mbarriers, flags)
 __host__ __device__ constexpr size_t clu_smem_bytes(int P) {
-    return sizeof(double) * (2 * (size_t)P + 32 + 2 * 32) + 2 * sizeof(unsigned long long) + 16;
+    return sizeof(double) * (2 * (size_t)P + 32 + 2 * 32) + 2 * sizeof(unsigned long long) + 16 +
+           sizeof(double) * (1 + kCluMaxK) + sizeof(unsigned long long);
 }
 // threads of one CTA: one owner warp (SEG <= 32 rows) + the GEMV teams
 __host__ __device__ constexpr int clu_threads(int seg, int team) {
@@ -149,6 +165,9 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
     unsigned long long *mbar = reinterpret_cast<unsigned long long *>(cps + 32 + 2 * 32);
     volatile int *sbad = reinterpret_cast<volatile int *>(mbar + 2);
     volatile long long *zslot = reinterpret_cast<volatile long long *>(mbar + 3);  // always 0
+    volatile int *sstop = reinterpret_cast<volatile int *>(mbar + 4);  // GEMV warps -> owners
+    double *sflg = reinterpret_cast<double *>(mbar + 5);  // [K] peers' "bad" words of a recording step
+    unsigned long long *fbar = mbar + 5 + kCluMaxK;       // mbarrier counting those words
 
     const int K = (int)clu_size(), b = (int)clu_rank();
     const int n = p.rows;
@@ -174,12 +193,14 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
     for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) xs[i] = 0.0;
     __syncthreads();
     for (int col = threadIdx.x; col < n; col += blockDim.x) xs[reg_xpos<C>(col, T)] = p.m[3 * (size_t)col];
-    const uint32_t bar0 = clu_u32(mbar), bar1 = clu_u32(mbar + 1);
+    const uint32_t bar0 = clu_u32(mbar), bar1 = clu_u32(mbar + 1), bar2 = clu_u32(fbar);
     if (threadIdx.x == 0) {
         clu_bar_init(bar0, 1);
         clu_bar_init(bar1, 1);
+        clu_bar_init(bar2, 1);
         *sbad = 0;
         *zslot = 0;
+        *sstop = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     V3 m{0.0, 0.0, 0.0}, s{0.0, 0.0, 0.0}, acc{0.0, 0.0, 0.0}, k3{0.0, 0.0, 0.0};
@@ -194,6 +215,7 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
     }
     clu_sync();  // every CTA's mbarriers and buffers are initialised before any st.async
     const uint32_t xbytes = 8u * (uint32_t)n;  // one 8-byte store per oscillator
+    const uint32_t fbytes = 8u * (uint32_t)K;  // + one "bad" word per CTA after a recording step
     const unsigned nthreads = blockDim.x;
     bool stop = false;
 
@@ -201,8 +223,12 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
         // ==================== GEMV teams ====================================
         if (t == 0) clu_expect(bar1, xbytes);  // x of stage 1
         long long next_rec = p.stride;
+        bool flags_in = false;  // the last step recorded: its "bad" words are checked at stage 1
+        uint32_t fphase = 0u;
+        long long next_flag = 0;
         for (long long step = 1; step <= p.steps && !stop; ++step) {
             const bool record = (step == next_rec) || (step == p.steps);
+            const bool fround = record && step < p.steps && step >= next_flag;  // a stop-flag round
 #pragma unroll
             for (int stage = 0; stage < 4; ++stage) {
                 [[maybe_unused]] const long long estage = (step - 1) * 4 + stage;
@@ -210,7 +236,23 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
                 if (!(step == 1 && stage == 0)) {
                     // phases of buffer 1: stages 1, 3 -> parity 0, 1; buffer 0: stages 2, 0 -> 0, 1
                     clu_wait(buf ? bar1 : bar0, (stage == 1 || stage == 2) ? 0u : 1u);
-                    if (t == 0) clu_expect(buf ? bar0 : bar1, xbytes);  // the next stage's buffer
+                    if (stage == 1 && flags_in) {  // cluster-wide stop decision (uniform)
+                        // the recording step's "bad" words (own mbarrier; they left with the
+                        // step's last x, long before this stage's x): one per lane, one vote
+                        clu_wait(bar2, fphase);
+                        fphase ^= 1u;
+                        const int fl = threadIdx.x & 31;
+                        if (__any_sync(0xffffffffu, fl < K && sflg[fl] != 0.0)) {
+                            if (t == 0) *sstop = 1;
+                            asm volatile("bar.arrive 1, %0;" ::"r"(nthreads) : "memory");
+                            stop = true;
+                            break;
+                        }
+                    }
+                    if (t == 0) {
+                        clu_expect(buf ? bar0 : bar1, xbytes);  // the next stage's buffer
+                        if (stage == 3 && fround) clu_expect(bar2, fbytes);
+                    }
                 }
                 CTL(estage, 3, t == 0, 0.0);
                 const double *xb = xs + buf * P;
@@ -232,12 +274,6 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
                 if (j == 0 && row < SEG) cps[row] = cp;
                 CTL(estage, 4, t == 0, cp);
                 asm volatile("bar.arrive 1, %0;" ::"r"(nthreads) : "memory");
-                if (stage == 3 && record) {  // cluster-wide stop decision (uniform branch)
-                    clu_sync();
-                    const uint32_t fl = clu_u32((const void *)sbad);
-                    for (int c = 0; c < K; ++c) stop |= clu_ld_s32(clu_mapa(fl, c)) != 0;
-                    if (stop) break;
-                }
                 if (!((step == p.steps) && stage == 3)) {
                     // publication fan-out: the owner warp staged this CTA's x in stg; GEMV
                     // warp gw sends it to CTAs gw, gw + nGW, ... (one 8-byte st.async per
@@ -252,6 +288,8 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
                     }
                 }
             }
+            flags_in = fround;
+            if (fround) next_flag = step + kCluFlagEvery;
             if (record && step == next_rec) next_rec += p.stride;
         }
     } else {
@@ -272,8 +310,11 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
         }
         long long next_rec = p.stride;
         long long rec_idx = 1;
+        bool flags_in = false, bad_seen = false;
+        long long next_flag = 0;
         for (long long step = 1; step <= p.steps && !stop; ++step) {
             const bool record = (step == next_rec) || (step == p.steps);
+            const bool fround = record && step < p.steps && step >= next_flag;  // a stop-flag round
 #pragma unroll
             for (int stage = 0; stage < 4; ++stage) {
                 [[maybe_unused]] const long long estage = (step - 1) * 4 + stage;
@@ -285,6 +326,10 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
                                "+d"(pre.bz), "+d"(pre.ax), "+d"(pre.ain_cin)
                              : "r"(nthreads)
                              : "memory");
+                if (stage == 1 && flags_in && *sstop) {  // the GEMV warps' stop decision
+                    stop = true;
+                    break;
+                }
                 CTL(estage, 0, threadIdx.x == 0, 0.0);
                 double xpub = 0.0;
                 bool bad = false;
@@ -320,14 +365,10 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
                     }
                 }
                 CTL(estage, 1, threadIdx.x == 0, xpub);
-                if (stage == 3 && record) {
-                    if (bad) *sbad = 1;
-                    clu_sync();
-                    const uint32_t fl = clu_u32((const void *)sbad);
-                    for (int c = 0; c < K; ++c) stop |= clu_ld_s32(clu_mapa(fl, c)) != 0;
-                    if (stop) break;
-                }
                 const bool last = (step == p.steps) && stage == 3;
+                if (stage == 3 && record) bad_seen |= __any_sync(0xffffffffu, bad);
+                if (stage == 3 && fround && r < K)  // this CTA's "bad" word into slot b of CTA r
+                    clu_st_async(clu_mapa(clu_u32(sflg + b), r), bad_seen ? 1.0 : 0.0, clu_mapa(bar2, r));
                 if (!last) {  // hand x to the GEMV warps, which send it (fan-out above)
                     if (owner) stg[r] = xpub;
                     asm volatile("bar.arrive 2, %0;" ::"r"(nthreads) : "memory");
@@ -356,6 +397,8 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
                     }
                 }
             }
+            flags_in = fround;
+            if (fround) next_flag = step + kCluFlagEvery;
             if (record && step == next_rec) {
                 next_rec += p.stride;
                 ++rec_idx;
@@ -386,7 +429,8 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_rk4_kernel(const _
 // clu_rk4_kernel: mbarrier wait -> GEMV + butterfly -> RHS post -> st.async.
 // ----------------------------------------------------------------------------
 __host__ __device__ constexpr size_t clu_hyb_smem_bytes(int P) {
-    return sizeof(double) * (2 * (size_t)P + 32 * 3 + 32 * 8) + 2 * sizeof(unsigned long long) + 16;
+    return sizeof(double) * (2 * (size_t)P + 32 * 3 + 32 * 8) + 2 * sizeof(unsigned long long) + 16 +
+           sizeof(double) * kCluMaxK + sizeof(unsigned long long);
 }
 
 template <int T, int C>
@@ -399,7 +443,10 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
     double *sst = xs + 2 * P;    // [32][3] stage point, teams -> owner warp
     double *spre = sst + 96;     // 256: own-state RHS half, owner warp -> teams ([8][32] if T <= 2, else [32][8])
     unsigned long long *mbar = reinterpret_cast<unsigned long long *>(spre + 256);
-    volatile int *sbad = reinterpret_cast<volatile int *>(mbar + 2);
+    volatile int *sbad = reinterpret_cast<volatile int *>(mbar + 2);   // a row of this CTA diverged
+    volatile int *sstop = reinterpret_cast<volatile int *>(mbar + 3);  // teams -> owner warp
+    double *sflg = reinterpret_cast<double *>(mbar + 4);  // [K] peers' "bad" words of a recording step
+    unsigned long long *fbar = mbar + 4 + kCluMaxK;       // mbarrier counting those words
 
     const int K = (int)clu_size(), b = (int)clu_rank();
     const int n = p.rows;
@@ -420,15 +467,18 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
     for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) xs[i] = 0.0;
     __syncthreads();
     for (int col = threadIdx.x; col < n; col += blockDim.x) xs[reg_xpos<C>(col, T)] = p.m[3 * (size_t)col];
-    const uint32_t bar0 = clu_u32(mbar), bar1 = clu_u32(mbar + 1);
+    const uint32_t bar0 = clu_u32(mbar), bar1 = clu_u32(mbar + 1), bar2 = clu_u32(fbar);
     if (threadIdx.x == 0) {
         clu_bar_init(bar0, 1);
         clu_bar_init(bar1, 1);
+        clu_bar_init(bar2, 1);
         *sbad = 0;
+        *sstop = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     clu_sync();  // every CTA's mbarriers and buffers are initialised before any st.async
     const uint32_t xbytes = 8u * (uint32_t)n;
+    const uint32_t fbytes = 8u * (uint32_t)K;  // + one "bad" word per CTA after a recording step
     auto u_of = [&](long long st) {  // drive sample of step `st` (zero-order hold, model.py:93-149)
         return p.n_samples > 1 ? p.samples + ((st - 1) / p.sps) * p.n_in : p.samples;
     };
@@ -448,17 +498,40 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
             }
         }
         const uint32_t xa0 = clu_u32(xs + b * SEG + row), xa1 = clu_u32(xs + P + b * SEG + row);
-        if (t == 0) clu_expect(bar1, xbytes);  // x of stage 1
+        // the x of stages 1 and 2; later phases are armed by the owner warp (below),
+        // off the teams' critical path
+        if (t == 0) {
+            clu_expect(bar1, xbytes);
+            clu_expect(bar0, xbytes);
+        }
         long long next_rec = p.stride, rec_idx = 1;
+        bool flags_in = false;  // the last step recorded: its "bad" words are checked at stage 1
+        uint32_t fphase = 0u;
+        long long next_flag = 0;
         for (long long step = 1; step <= p.steps && !stop; ++step) {
             const bool record = (step == next_rec) || (step == p.steps);
+            const bool fround = record && step < p.steps && step >= next_flag;  // a stop-flag round
 #pragma unroll
             for (int stage = 0; stage < 4; ++stage) {
                 [[maybe_unused]] const long long estage = (step - 1) * 4 + stage;
                 const int buf = stage & 1;
                 if (!(step == 1 && stage == 0)) {
                     clu_wait(buf ? bar1 : bar0, (stage == 1 || stage == 2) ? 0u : 1u);
-                    if (t == 0) clu_expect(buf ? bar0 : bar1, xbytes);
+                    if (stage == 1 && flags_in) {  // cluster-wide stop decision (uniform)
+                        // the recording step's "bad" words (own mbarrier; they left with the
+                        // step's last x, long before this stage's x): one per lane, one vote
+                        clu_wait(bar2, fphase);
+                        fphase ^= 1u;
+                        const int fl = threadIdx.x & 31;
+                        if (__any_sync(0xffffffffu, fl < K && sflg[fl] != 0.0)) {
+                            // consume the owner warp's pending hand-off, then release it
+                            asm volatile("bar.sync 3, %0;" ::"r"(nthreads) : "memory");
+                            if (t == 0) *sstop = 1;
+                            asm volatile("bar.arrive 4, %0;" ::"r"(nthreads) : "memory");
+                            stop = true;
+                            break;
+                        }
+                    }
                 }
                 CTL(estage, 3, t == 0, 0.0);
                 const double *xb = xs + buf * P;
@@ -537,13 +610,7 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
                     }
                 }
                 CTL(estage, 1, t == 0, xpub);
-                if (stage == 3 && record) {  // cluster-wide stop decision (uniform branch)
-                    if (bad) *sbad = 1;
-                    clu_sync();
-                    const uint32_t fl = clu_u32((const void *)sbad);
-                    for (int c = 0; c < K; ++c) stop |= clu_ld_s32(clu_mapa(fl, c)) != 0;
-                    if (stop) break;
-                }
+                if (bad) *sbad = 1;  // sticky; the owner warp sends it on the next stop-flag round
                 if (!((step == p.steps) && stage == 3)) {
                     const int nb = (stage + 1) & 1;
                     if (live)
@@ -560,6 +627,8 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
                     asm volatile("bar.arrive 4, %0;" ::"r"(nthreads) : "memory");
                 }
             }
+            flags_in = fround;
+            if (fround) next_flag = step + kCluFlagEvery;
             if (record && step == next_rec) {
                 next_rec += p.stride;
                 ++rec_idx;
@@ -607,24 +676,35 @@ __global__ void __launch_bounds__(C >= 32 ? 288 : 576, 1) clu_hyb_kernel(const _
         put(row_rhs_pre(m0, cin, p.c));
         asm volatile("bar.arrive 3, %0;" ::"r"(nthreads) : "memory");
         long long next_rec = p.stride;
+        bool flags_in = false;
+        long long next_flag = 0;
         for (long long step = 1; step <= p.steps && !stop; ++step) {
             const bool record = (step == next_rec) || (step == p.steps);
+            const bool fround = record && step < p.steps && step >= next_flag;  // a stop-flag round
 #pragma unroll
             for (int stage = 0; stage < 4; ++stage) {
-                if (stage == 3 && record) {  // the teams' stop decision, same barrier
-                    clu_sync();
-                    const uint32_t fl = clu_u32((const void *)sbad);
-                    for (int c = 0; c < K; ++c) stop |= clu_ld_s32(clu_mapa(fl, c)) != 0;
-                    if (stop) break;
-                }
                 if ((step == p.steps) && stage == 3) break;
                 if (stage == 0 && p.n_in == 1 && step < p.steps) u_next = u_of(step + 1)[0];  // prefetch
                 asm volatile("bar.sync 4, %0;" ::"r"(nthreads) : "memory");
+                if (stage == 1 && flags_in && *sstop) {  // the teams' stop decision
+                    stop = true;
+                    break;
+                }
+                // the teams are done with stage `stage`, so its buffer's phase has
+                // completed here: arm that buffer for stage + 2 (stage 0 of step 1
+                // read the local initial x; stage 2's phase was armed up front)
+                if (r == 0 && !(step == 1 && stage == 0)) clu_expect((stage & 1) ? bar1 : bar0, xbytes);
+                if (stage == 3 && fround) {  // this CTA's (sticky) "bad" word into slot b of CTA r
+                    if (r == 0) clu_expect(bar2, fbytes);
+                    if (r < K) clu_st_async(clu_mapa(clu_u32(sflg + b), r), *sbad ? 1.0 : 0.0, clu_mapa(bar2, r));
+                }
                 const V3 v = r < SEG ? V3{sst[3 * r], sst[3 * r + 1], sst[3 * r + 2]} : V3{0.0, 0.0, 0.0};
                 if (stage == 3) cin = p.n_in == 1 ? rmul(win, u_next) : cin_of(step + 1);
                 put(row_rhs_pre(v, cin, p.c));
                 asm volatile("bar.arrive 3, %0;" ::"r"(nthreads) : "memory");
             }
+            flags_in = fround;
+            if (fround) next_flag = step + kCluFlagEvery;
             if (record && step == next_rec) next_rec += p.stride;
         }
     }

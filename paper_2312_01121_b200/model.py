@@ -132,19 +132,46 @@ def total_b(m, u, topology, params, consts=None) -> np.ndarray:
     return b
 
 
+_BACKENDS: dict = {}  # id(topology) -> (weakref(topology), {scalars: B200Backend})
+
+
+def _backend_for(topology, scalars: tuple):
+    """One B200 plan per (topology, kernel scalars), reused across calls: the W
+    upload and layout permute happen once, like the reference's TorchBackend
+    copying W at construction (gpu.py:68-71).  Entries die with the topology."""
+    import weakref
+
+    from .backends.b200 import B200Backend
+
+    key = id(topology)
+    hit = _BACKENDS.get(key)
+    if hit is None or hit[0]() is not topology:
+        hit = (weakref.ref(topology, lambda _r, k=key: _BACKENDS.pop(k, None)), {})
+        _BACKENDS[key] = hit
+    plans = hit[1]
+    if scalars not in plans:
+        if len(plans) >= 4:  # a parameter sweep through this helper: keep the newest few
+            plans.pop(next(iter(plans))).close()
+        plans[scalars] = B200Backend(topology, None, consts=scalars)
+    return plans[scalars]
+
+
 def llg_derivative(m, u, topology, params, consts=None, out=None, workspace=None):
     """dm/dt for the whole array, evaluated by the K0 kernel on the GPU.
 
     Same contract as ref `model.py:206-302`: writes only `out` (allocated when
-    None). `consts` and `workspace` are accepted for signature compatibility;
-    the device plan owns its scratch.
+    None); `consts` (a DerivedConstants) replaces `derive(params)` as in the
+    reference.  The device plan for (topology, scalars) is cached, so repeated
+    calls pay only the m/u/out copies.  `workspace` is accepted for signature
+    compatibility; the device plan owns its scratch.
     """
-    from .backends.b200 import B200Backend
+    from .params import kernel_scalars
 
     m = np.ascontiguousarray(np.asarray(m, dtype=np.float64))
     if out is None:
         out = np.empty_like(m)
-    B200Backend(topology, params).derivative(m, np.asarray(u, dtype=np.float64), out)
+    backend = _backend_for(topology, tuple(float(v) for v in kernel_scalars(params, consts)))
+    backend.derivative(m, np.asarray(u, dtype=np.float64), out)
     return out
 
 

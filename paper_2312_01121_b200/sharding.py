@@ -164,6 +164,49 @@ def shard_members(batch: int, world: int, rank: int) -> np.ndarray:
     return np.array_split(np.arange(batch), world)[rank]
 
 
+def integrate_ensemble_sharded(backend, consts: np.ndarray, samples: np.ndarray,
+                               steps_per_sample: int, config, group) -> np.ndarray:
+    """Batch-sharded ensemble: this rank's members on its own
+    GPU, then one all-gather of the recorded grids.  consts (B, 11) and
+    samples ([B,] n_samples, n_in) describe the WHOLE batch; returns the
+    (R, B, n, 3) grid on every rank (see integrate_ensemble)."""
+    import torch.distributed as dist
+
+    from .topology import initial_state
+
+    group = None if group == "world" else group
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    batch = consts.shape[0]
+    if batch < world:
+        raise ParameterError(f"cannot batch-shard {batch} members over {world} ranks")
+    mine = shard_members(batch, world, rank)
+    counts = [(0, len(shard_members(batch, world, r))) for r in range(world)]
+    samples_mine = samples[mine] if samples.ndim == 3 else samples
+    m = np.tile(initial_state(config.n, config.phi0)[None], (len(mine), 1, 1))
+    local_error = None
+    states = None
+    try:
+        states = backend.integrate_ensemble_run(consts[mine], samples_mine, steps_per_sample,
+                                                config.dt, config.steps, config.record_stride, m)
+        status = (RUN_OK, 0, 0)
+    except IntegrationDivergedError as exc:
+        # step, then global member, then oscillator: packed so min() keeps that order
+        member = int(mine[0]) + int(getattr(exc, "member", 0))
+        status = (RUN_DIVERGED, member * (1 << 32) + exc.oscillator, exc.step)
+    except SpinoscError as exc:
+        status, local_error = (RUN_FAILED, 0, 0), exc
+    try:
+        agree_status(status, group, local_error)
+    except IntegrationDivergedError as exc:
+        err = IntegrationDivergedError(oscillator=exc.oscillator & 0xffffffff, step=exc.step)
+        err.member = exc.oscillator >> 32
+        raise err from None
+    import torch
+
+    block = torch.as_tensor(states).to(collective_device(group))
+    return gather_rows(block, counts, batch, group).cpu().numpy()
+
+
 class ShardedB200Backend:
     """One rank of a row-sharded trajectory (one process per GPU, torch.distributed).
 

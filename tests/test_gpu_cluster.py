@@ -98,6 +98,42 @@ def test_divergence_reported_by_every_cluster_size(monkeypatch, name):
         be.close()
 
 
+@pytest.mark.parametrize("stride", [1, 3, 7, 70])
+@pytest.mark.parametrize("hyb", ["1", "0"])
+def test_divergence_between_stop_flag_rounds(monkeypatch, oracle_mod, stride, hyb):
+    """The cluster stops on stop-flag rounds (at most one per kCluFlagEvery = 64
+    steps), not on every recording step: a row that goes non-finite between
+    rounds is still reported at ITS recording step, first oscillator first
+    (integrator.py:174-177), and the run stops on the next round.  Late
+    divergence of traj_n6_diverge_late's reservoir, embedded in n = 100 / 200
+    (the other rows decoupled), at record strides that put it between rounds."""
+    import paper_2312_01121_b200 as sto
+
+    d = load_golden("traj_n6_diverge_late.npz")
+    monkeypatch.setenv("STO_CLU_HYB", hyb)
+    n = 100 if hyb == "1" else 200
+    w = np.zeros((n, n))
+    w[:6, :6] = d["w"]
+    w_in = np.zeros((n, 1))
+    w_in[:6] = d["w_in"]
+    top = sto.Topology(sto.CouplingMatrix(w), sto.InputWeights(w_in))
+    m0 = sto.initial_state(n)
+    m0[:6] = d["m0"]
+    steps, sps = int(d["steps"]), int(d["steps_per_sample"])
+    with pytest.raises(oracle_mod.OracleDiverged) as want:
+        oracle_mod.integrate(w, w_in, d["consts"], m0, d["samples"], sps, float(d["dt"]), steps,
+                             stride)
+    for k in (2, 8):
+        if (k, 32) not in _variants(n):
+            continue
+        be = _backend(sto, top, monkeypatch, k, 32, consts=d["consts"])
+        with pytest.raises(sto.IntegrationDivergedError) as info:
+            be.integrate_run(m0.copy(), d["samples"], sps, float(d["dt"]), steps, stride)
+        assert (info.value.oscillator, info.value.step) == (want.value.oscillator,
+                                                           want.value.step), (k, stride)
+        be.close()
+
+
 def test_golden_config1_through_cluster(monkeypatch):
     """configs[0] (N = 100, 1e4 steps, a new drive sample every step): the
     reference's own trajectory, every cluster size."""

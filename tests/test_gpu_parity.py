@@ -141,6 +141,29 @@ def test_derivative_golden(sto):
         assert_bit_equal(got, z[key + "_out"], f"llg_derivative {key}")
 
 
+def test_llg_derivative_consts_and_plan_cache(sto, oracle_mod):
+    """model.llg_derivative honours a caller-supplied DerivedConstants (ref
+    model.py:206-230) and reuses one device plan per (topology, scalars)."""
+    from paper_2312_01121_b200 import model
+
+    n = 300
+    top = sto.build_topology(n, seed=4)
+    p0, p1 = sto.PhysicalParams(), sto.PhysicalParams(current=2.5e-3)
+    g = np.random.default_rng(4)
+    m = g.normal(size=(n, 3))
+    m /= np.linalg.norm(m, axis=1, keepdims=True)
+    u = g.uniform(-1, 1, 1)
+    want = oracle_mod.derivative(top.coupling.entries, top.input_weights.entries,
+                                 sto.kernel_scalars(p1), m, u)
+    got = sto.llg_derivative(m, u, top, p0, consts=sto.derive(p1))  # consts win over params
+    assert_bit_equal(got, want, "llg_derivative(consts=)")
+    before = len(model._BACKENDS[id(top)][1])
+    for _ in range(3):
+        again = sto.llg_derivative(m, u, top, p1)
+    assert_bit_equal(again, want, "llg_derivative(params)")
+    assert len(model._BACKENDS[id(top)][1]) == before  # same scalars: the cached plan
+
+
 def test_derivative_on_device_tensors(sto):
     import torch
 

@@ -108,12 +108,39 @@ def test_ipc_transport_multiprocess(world, n):
     assert res["ok"] and res["world"] == world, res
 
 
-def test_bench_multirank_path_on_one_gpu():
-    """bench.py --gpus 2 under torchrun (STO_BENCH_SHARE_GPU: both ranks on cuda:0,
-    gloo): the row-sharded n1e4 path -- ShardedB200Backend construction, IPC
-    connect, timed runs, max-over-ranks, e2e -- prints one valid JSON line."""
+@pytest.mark.parametrize("workload", ["n1e4", "ens512"])
+def test_bench_multirank_path_on_one_gpu(workload):
+    """`bench.py --gpus 2` with no external torchrun (it spawns its own ranks;
+    STO_BENCH_SHARE_GPU puts both on cuda:0 with gloo): the row-sharded n1e4
+    path -- ShardedB200Backend construction, IPC connect, timed runs,
+    max-over-ranks, e2e with the device-side gather -- and the batch-sharded
+    ensemble through integrate_ensemble(group=), each printing one valid line
+    with n_gpus == 2."""
     import json
     import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, STO_BENCH_SHARE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--workload", workload,
+           "--steps", "1", "--warmup", "1", "--rk4-steps", "4", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert out.returncode == 0 and len(lines) == 1, out.stdout[-2000:] + out.stderr[-3000:]
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    want = "row-sharded" if workload == "n1e4" else "batch-sharded"
+    assert want in line["config"]["parallelism"]
+
+
+def test_sharded_ensemble_matches_single_gpu():
+    """integrate_ensemble(group=) over 2 ranks (torchrun, both on cuda:0, gloo)
+    returns every member on every rank, bit-identical to the one-GPU ensemble
+    of the same members (members are independent; the same kernel runs them)."""
+    import json
     import socket
     import subprocess
     import sys
@@ -123,15 +150,14 @@ def test_bench_multirank_path_on_one_gpu():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    env = dict(os.environ, STO_BENCH_SHARE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
-           "--gpus", "2", "--steps", "1", "--warmup", "1", "--rk4-steps", "4", "--no-cpu-baseline"]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(ROOT / "tools" / "ens_shard_selftest.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
-    assert out.returncode == 0 and len(lines) == 1, out.stdout[-2000:] + out.stderr[-3000:]
-    line = json.loads(lines[0])
-    assert line["n_gpus"] == 2 and line["value"] > 0 and "row-sharded" in line["config"]["parallelism"]
+    assert out.returncode == 0 and lines, out.stdout[-2000:] + out.stderr[-3000:]
+    res = json.loads(lines[-1])
+    assert res["ok"], res
 
 
 from hypothesis import HealthCheck, given, settings  # noqa: E402

@@ -33,6 +33,10 @@ CASES = {
     "cluster_own_k16_n200": ("cluster", 200, 4, 2, {"STO_CLU_HYB": "0", "STO_CLU_K": "16"}),
     "cluster_hyb_k16_n200": ("cluster", 200, 4, 2, {"STO_CLU_HYB": "1", "STO_CLU_K": "16"}),
     "cluster_c64_n400": ("cluster", 400, 3, 1, {}),
+    # the record-step stop path (divergence words on the mbarrier, no cluster barrier)
+    "cluster_hyb_k8_n100_div": ("cluster", 100, 6, 1, {"STO_CLU_HYB": "1", "SAN_DIVERGE": "1"}),
+    "cluster_own_k16_n200_div": ("cluster", 200, 6, 1, {"STO_CLU_HYB": "0", "STO_CLU_K": "16",
+                                                        "SAN_DIVERGE": "1"}),
     "reg_single_n100": ("reg", 100, 4, 2, {}),
     "reg_grid_n700": ("reg", 700, 3, 1, {}),
     "single_n60": ("single", 60, 4, 2, {}),
@@ -102,6 +106,19 @@ def main(name: str) -> None:
         from paper_2312_01121_b200.backends.b200 import B200Backend
 
         be = B200Backend(top, p, device=0, flags=FORCE[fam])
+        if os.environ.get("SAN_DIVERGE") == "1":  # a bad oscillator: every CTA must stop
+            bad = m0.copy()
+            bad[n // 2] = (1e200, 1e200, 1e200)
+            try:
+                oracle.integrate(w, w_in, consts, bad, drive, 1, 1e-11, steps, stride)
+                raise AssertionError("oracle did not diverge")
+            except oracle.OracleDiverged as e:
+                want_div = (e.oscillator, e.step)
+            try:
+                be.integrate_run(bad, drive, 1, 1e-11, steps, stride)
+                raise AssertionError("no divergence reported")
+            except sto.IntegrationDivergedError as e:
+                assert (e.oscillator, e.step) == want_div, ((e.oscillator, e.step), want_div)
         m = m0.copy()
         got = be.integrate_run(m, drive, 1, 1e-11, steps, stride)
         want, _ = oracle.integrate(w, w_in, consts, m0, drive, 1, 1e-11, steps, stride)
