@@ -214,6 +214,14 @@ STO_API int sto_gemv(int device, const double *w, int64_t rows, int64_t cols, in
 /* a[i] /= divisor (IEEE), device, asynchronous: `entries /= rho`. */
 STO_API int sto_scale_div(int device, double *a, int64_t count, double divisor, void *stream);
 
+/* Self-test of the kernels' speculative division (sto_device.cuh rdiv_spec, used
+ * for h_s = pref / (1 + lambda m.p), model.py:250 / cpu_jit.py:68): for each i,
+ * q[i] = rdiv_spec(a[i], b[i]) and ok[i] = its proof of correct rounding, and
+ * ref[i] = __ddiv_rn(a[i], b[i]).  Test hook only (tests/test_gpu_division.py):
+ * ok[i] = 1 must imply q[i] == ref[i] bit for bit.  Device pointers, async. */
+STO_API int sto_selftest_div(int device, const double *a, const double *b, int64_t count, double *q,
+                             int32_t *ok, double *ref, void *stream);
+
 /* Recorded states as CSV text (integrator.py:217-225 write_trajectory_csv):
  * header "t,k,mx,my,mz", then one row per (record i, oscillator k) in that
  * order, every float as Python's f"{x:.17g}" (byte-identical), formatted by

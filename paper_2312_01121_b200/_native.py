@@ -105,6 +105,9 @@ SIGNATURES = {
                                 ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "sto_scale_div": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.c_double, ctypes.c_void_p]),
+    "sto_selftest_div": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p]),
     "sto_write_trajectory_csv": (ctypes.c_int, [ctypes.c_char_p, _c_double_p, _c_double_p,
                                                 ctypes.c_int64, ctypes.c_int64, ctypes.c_int32]),
 }
@@ -208,6 +211,19 @@ def scale_div(a, divisor: float) -> None:
     """a /= divisor in place (IEEE division) on the device."""
     dev = a.device.index
     check(lib().sto_scale_div(dev, a.data_ptr(), a.numel(), float(divisor), _stream_ptr(dev)))
+
+
+def selftest_div(a, b):
+    """(q, ok, ref) of the kernels' speculative division vs __ddiv_rn (test hook)."""
+    import torch
+
+    dev = a.device.index
+    q = torch.empty_like(a)
+    ref = torch.empty_like(a)
+    ok = torch.empty(a.shape, dtype=torch.int32, device=a.device)
+    check(lib().sto_selftest_div(dev, a.data_ptr(), b.data_ptr(), a.numel(), q.data_ptr(),
+                                 ok.data_ptr(), ref.data_ptr(), _stream_ptr(dev)))
+    return q, ok, ref
 
 
 class Plan:

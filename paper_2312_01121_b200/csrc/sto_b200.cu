@@ -650,6 +650,8 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
             }
         }
         P->grid = g;
+        if (P->rows_cap > P->chunk_cols)  // the row phase stages the x slice in the X window
+            return bail(fail(STO_E_PARAM, "sharded plan: more rows per CTA than the x window holds"));
     } else if (n <= 32 && !(fl & STO_PLAN_NO_TINY) && !forced) {
         P->kind = kTiny;
         P->grid = 1;
@@ -1085,7 +1087,8 @@ int sto_integrate_group(sto_plan **plans, int32_t world, const sto_run *r, sto_s
     p.rows_cap = cap;
     p.chunk_cols = P0->chunk_cols;
     const size_t smem = grid_smem(cap, P0->L.cs, p.chunk_cols, P0->kind == kResident);
-    if (smem > kSmemBudget) return fail(STO_E_PARAM, "group shard does not fit shared memory");
+    if (smem > kSmemBudget || cap > p.chunk_cols)
+        return fail(STO_E_PARAM, "group shard does not fit shared memory");
     p.mp.world = world;
     p.mp.rank_base = 0;
     p.mp.ctas_per_rank = per;
@@ -1274,6 +1277,15 @@ int sto_scale_div(int device, double *a, int64_t count, double divisor, void *st
     if (!a || count < 0) return fail(STO_E_PARAM, "sto_scale_div: bad arguments");
     STO_CUDA(cudaSetDevice(device));
     scale_div_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(a, count, divisor);
+    STO_CUDA(cudaGetLastError());
+    return STO_OK;
+}
+
+int sto_selftest_div(int device, const double *a, const double *b, int64_t count, double *q,
+                     int32_t *ok, double *ref, void *stream) {
+    if (!a || !b || !q || !ok || !ref || count < 0) return fail(STO_E_PARAM, "sto_selftest_div: bad arguments");
+    STO_CUDA(cudaSetDevice(device));
+    selftest_div_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(a, b, count, q, ok, ref);
     STO_CUDA(cudaGetLastError());
     return STO_OK;
 }

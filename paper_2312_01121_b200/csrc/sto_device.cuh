@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace sto {
@@ -25,6 +26,50 @@ __device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// Correctly rounded a/b without the library division's on-chain range check.
+//
+// __ddiv_rn costs ~113 cycles of dependent latency (profiles/r01_microbench.json),
+// most of it the MUFU seed, three Newton/FMA corrections and a range test whose
+// branch sits in front of every consumer.  Here the quotient comes from a
+// shorter chain (seed -> e -> e+e^2 -> q0 -> remainder -> q: the seed plus
+// five DFMA) and its correctness is *proved* afterwards, off the chain:
+//   * q == RN(a/b) iff |a/b - q| < half the spacing of doubles on a/b's side
+//     of q, i.e. |a - b*q| < |b| * ulp(q)/2 (ulp(q)/4 when q is a power of two,
+//     conservatively, so the narrower gap below 2^k is used on both sides);
+//     an exact midpoint is impossible for a quotient of two doubles (away from
+//     underflow), so the comparison is strict;
+//   * a - b*q is exact in one FMA whenever |q - a/b| <= 1 ulp (the remainder is
+//     a multiple of ulp(b)*ulp(q) of magnitude < |b|*ulp(q): it fits 53 bits);
+//     a q off by more fails the test by a wide margin either way;
+//   * the exponent guards keep every quantity above (q, b, b*ulp/2, the
+//     remainder) normal and finite; outside them, or for NaN/inf/0, ok = false.
+// The caller must redo the work with rdiv() when ok is false (the kernels
+// replay the whole RK4 step; in practice it never triggers, see
+// sto_selftest_div).  IEEE division is unique, so the bits equal __ddiv_rn's.
+__device__ __forceinline__ double rdiv_spec(double a, double b, bool &ok) {
+    double r0;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(b));
+    const double e = __fma_rn(-b, r0, 1.0);
+    const double ar0 = __dmul_rn(a, r0);
+    const double pe = __fma_rn(e, e, e);
+    const double y = __fma_rn(r0, pe, r0);
+    const double q0 = __fma_rn(ar0, pe, ar0);
+    const double rem = __fma_rn(-b, q0, a);
+    const double q = __fma_rn(rem, y, q0);
+    // ---- proof of correct rounding (independent of the chain above) ----
+    const double rem2 = __fma_rn(-b, q, a);
+    const long long qb = __double_as_longlong(q);
+    const long long bb = __double_as_longlong(b);
+    const unsigned eq = (unsigned)(qb >> 52) & 0x7ffu;
+    const unsigned eb = (unsigned)(bb >> 52) & 0x7ffu;
+    // ulp(q)/2 as a double: exponent eq - 53 (eq - 54 for a power of two)
+    const unsigned eh = eq - 53u - ((qb & 0xfffffffffffffLL) == 0 ? 1u : 0u);
+    const double half_ulp = __longlong_as_double((long long)eh << 52);
+    const double lim = __dmul_rn(fabs(b), half_ulp);
+    ok = (eq - 400u < 1200u) & (eb - 823u < 400u) & (fabs(rem2) < lim);  // 2^-623 <= |q| < 2^577, 2^-200 <= |b| < 2^200
+    return q;
+}
 
 struct Consts {
     double c_prec, c_damp, h_appl, h_aniso, pref, lam, a_cp, a_in, px, py, pz;
@@ -45,10 +90,20 @@ struct RhsPre {
     double hs_qx, by, bz, ax, ain_cin;
 };
 
-__device__ __forceinline__ RhsPre row_rhs_pre(V3 m, double cin, const Consts &c) {
+// kSpec: the division goes through rdiv_spec and `ok` collects its proof
+// (the caller replays the step with kSpec = false when any proof failed).
+template <bool kSpec = false>
+__device__ __forceinline__ RhsPre row_rhs_pre(V3 m, double cin, const Consts &c, bool *ok = nullptr) {
     double md = radd(rmul(m.x, c.px), rmul(m.y, c.py));
     md = radd(md, rmul(m.z, c.pz));
-    const double hs = rdiv(c.pref, radd(1.0, rmul(c.lam, md)));
+    double hs;
+    if constexpr (kSpec) {
+        bool good;
+        hs = rdiv_spec(c.pref, radd(1.0, rmul(c.lam, md)), good);
+        *ok = *ok & good;
+    } else {
+        hs = rdiv(c.pref, radd(1.0, rmul(c.lam, md)));
+    }
     const double qx = rsub(rmul(c.py, m.z), rmul(c.pz, m.y));
     const double qy = rsub(rmul(c.pz, m.x), rmul(c.px, m.z));
     const double qz = rsub(rmul(c.px, m.y), rmul(c.py, m.x));
@@ -77,8 +132,9 @@ __device__ __forceinline__ V3 row_rhs_post(const RhsPre &r, double cp, const Con
     return d;
 }
 
-__device__ __forceinline__ V3 row_rhs(V3 m, double cp, double cin, const Consts &c) {
-    return row_rhs_post(row_rhs_pre(m, cin, c), cp, c);
+template <bool kSpec = false>
+__device__ __forceinline__ V3 row_rhs(V3 m, double cp, double cin, const Consts &c, bool *ok = nullptr) {
+    return row_rhs_post(row_rhs_pre<kSpec>(m, cin, c, ok), cp, c);
 }
 
 // s = m + k*h   (integrator.py:107-108, 110-111, 113-114)

@@ -90,7 +90,7 @@ __host__ __device__ constexpr int ens_slot_doubles(int u) { return 8 * u * kEnsK
 __host__ __device__ constexpr size_t ens_smem_bytes(int u) {
     return sizeof(double) * ((size_t)kEnsGroups * kEnsSlots * ens_slot_doubles(u) + 8 * u * kEnsLDB +
                              kEnsBT * 11 + 8 * u) +
-           sizeof(unsigned long long) * 2 * kEnsGroups * kEnsSlots + 16;  // barriers, counters, TMEM base, flag
+           sizeof(unsigned long long) * 2 * kEnsGroups * kEnsSlots + 16;  // barriers, counters, TMEM base, gate, stop[2]
 }
 static_assert(ens_smem_bytes(kEnsMaxU) <= 227 * 1024, "ensemble shared memory budget");
 
@@ -171,6 +171,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_cta(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v)
+                 : "memory");
+    return old;
 }
 __device__ __forceinline__ void group_sync(int grp) {  // named barrier 1 + grp over one warp group
     asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kEnsGroupThreads) : "memory");
@@ -279,6 +285,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
     unsigned *done_all = reinterpret_cast<unsigned *>(full_all + kEnsGroups * kEnsSlots);
     uint32_t *tmem_base_slot = done_all + kEnsGroups * kEnsSlots;
     volatile int *go = reinterpret_cast<volatile int *>(tmem_base_slot + 1);  // group 1 start gate
+    volatile int *stop_grp = go + 1;  // [2] per group: stop after this recording step
 
     const int rt = blockIdx.x % p.n_rt, ct = blockIdx.x / p.n_rt;  // row tile, member column
     const int row0 = rt * TR, col0 = ct * kEnsBT;
@@ -338,7 +345,10 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
     };
     // first warp of the group: wait until every row tile has published this half-column's
     // x of stage g (counter >= (g+1) * n_rt), then issue the X parts of the ring's first chunks.
-    auto open_stage = [&](long long g) {
+    // Returns the half-column's stop word (read after the counter, so every row
+    // tile of the half-column reads the same value; see the record-step stop below).
+    auto open_stage = [&](long long g) -> unsigned long long {
+        unsigned long long stop = 0;
         if (lane == 0) {
             const unsigned long long target = (unsigned long long)(g + 1) * p.n_rt;
             unsigned long long v;
@@ -349,10 +359,12 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
             }
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
             asm volatile("fence.proxy.async.global;" ::: "memory");
+            stop = *((volatile unsigned long long *)bar + 1);
         }
         __syncwarp();
         const int s0 = (int)((g * n_chunks) % nring);
         if (lane < nring) issue_x((s0 + lane) % nring, lane, g);
+        return __shfl_sync(0xffffffffu, stop, 0);
     };
 
     // ---- roles -------------------------------------------------------------------
@@ -466,12 +478,14 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
                     }
                 }
                 // Slot consumed by this warp; the LAST of the group's warps to get here
-                // refills it (the slot's shared-memory reads are complete: their values
-                // fed the DMMAs above, so a relaxed counter suffices).  A chunk of the
-                // next stage gets only its W here; its X follows in open_stage.
+                // refills it.  The counter is an acq_rel atomic: every warp's fragment
+                // loads of the slot (ordered before its increment by __syncwarp)
+                // happen-before the last warp's refill, whose async-proxy writes are
+                // ordered after its generic-proxy view by fence.proxy.async.  A chunk
+                // of the next stage gets only its W here; its X follows in open_stage.
                 __syncwarp();
                 if (lane == 0) {
-                    if (atomicAdd(&done[slot], 1u) % GW == GW - 1 && g_fill < n_stages) {
+                    if (atom_add_acq_rel_cta(&done[slot], 1u) % GW == GW - 1 && g_fill < n_stages) {
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         issue_w(slot, ch_fill);
                         if (g_fill == gstage) issue_x(slot, ch_fill, g_fill);
@@ -586,13 +600,43 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
             tmem_wait_st();
             ENS_TL(gstage, 2);
             if (!last_stage) {
+                // Record-step stop (integrator.py:174-177: the run ends at the first
+                // recording step with a non-finite state).  Each group ORs "a
+                // divergence at a step <= this one is known" (its own, or another
+                // CTA's already in the status key) into its half-column's stop word
+                // BEFORE its release increment; the word is read after the
+                // counter's acquire, so all row tiles of the half-column read the
+                // OR of every contribution and stop together.  Half-columns are
+                // not in lockstep: one that is behind keeps going until it reaches
+                // the known divergence step, so an earlier divergence of its own
+                // members is still found (the reported key stays the minimum).
+                // A stale key read is larger, i.e. only delays the stop.
+                const bool chk = stage == 3 && record;
                 group_sync(grp);  // this group's x rows are written; its cpb half is free again
                 if (wl == 0) {
                     if (lane == 0) {
+                        if (chk && (*((volatile long long *)&p.status->key) >> 40) <= step)
+                            atomicOr(bar + 1, 1ull);
                         __threadfence();
                         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
                     }
-                    open_stage(gstage + 1);
+                    const unsigned long long stop = open_stage(gstage + 1);
+                    if (chk && lane == 0) stop_grp[grp] = (int)stop;
+                }
+                if (chk) {
+                    group_sync(grp);
+                    if (stop_grp[grp]) {
+                        // drain: the ring's slots of the next stage are armed (their X
+                        // was just issued); wait for every copy before leaving
+                        for (int i = 0; i < nring; ++i) {
+                            mbar_wait(&full[slot], phase);
+                            if (++slot == nring) {
+                                slot = 0;
+                                phase ^= 1;
+                            }
+                        }
+                        goto done;
+                    }
                 }
             }
         }
@@ -601,6 +645,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
             ++rec_idx;
         }
     }
+done:
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");

@@ -323,8 +323,19 @@ __global__ void __launch_bounds__(NT, 1) grid_rk4_kernel(const __grid_constant__
                                                              : p.m[3 * (size_t)k];
                         xs[col_perm(cs, k) - x_base] = v;
                     }
+                } else if constexpr (MULTI) {
+                    // the receive buffer is in LOGICAL order (each rank pushes its
+                    // contiguous row slice as 16-byte vectors); the physical window
+                    // [x_base, x_base + x_len) holds exactly the logical columns of the
+                    // same range (segments are contiguous), permuted -- scatter them,
+                    // +0.0 for the padding columns k >= n
+                    const double *src = xrecv + (size_t)((p.mp.epoch_base + e) & 1) * cs.ldw;
+                    for (int i = threadIdx.x; i < x_len; i += blockDim.x) {
+                        const int k = x_base + i;
+                        xs[col_perm(cs, k) - x_base] = (k < cs.n) ? __ldcg(src + k) : 0.0;
+                    }
                 } else {
-                    const double *src = xrecv + (size_t)((MULTI ? p.mp.epoch_base + e : e) & 1) * cs.ldw + x_base;
+                    const double *src = xrecv + (size_t)(e & 1) * cs.ldw + x_base;
                     const double2 *src2 = reinterpret_cast<const double2 *>(src);
                     double2 *dst2 = reinterpret_cast<double2 *>(xs);
 #pragma unroll 4
@@ -415,10 +426,34 @@ __global__ void __launch_bounds__(NT, 1) grid_rk4_kernel(const __grid_constant__
                 }
             }
             if constexpr (MULTI) {
-                const int pos = col_perm(cs, k);
-                for (int q = 0; q < p.mp.world; ++q) p.mp.xbuf_of[q][par_next + pos] = xpub;
+                xs[r] = xpub;  // staged: the X window is free during the row phase
             } else {
                 xnext[col_perm(cs, k)] = xpub;
+            }
+        }
+        if constexpr (MULTI) {
+            // push this CTA's contiguous slice [k0, k0 + nrow) of the stage x into
+            // every rank's receive buffer (logical order) as 16-byte stores: one
+            // scalar head when k0 is odd, pairs, one scalar tail -- instead of
+            // nrow scattered 8-byte stores per peer
+            __syncthreads();
+            if (integrate) {
+                const long long k0 = rb + r0;
+                const int head = (int)(k0 & 1) < nrow ? (int)(k0 & 1) : 0;
+                const int npair = (nrow - head) >> 1;
+                const int per = head + npair + ((nrow - head) & 1);
+                for (int i = threadIdx.x; i < per * p.mp.world; i += blockDim.x) {
+                    const int q = i / per, j = i - q * per;
+                    double *dst = p.mp.xbuf_of[q] + par_next + k0;
+                    if (j < head) {
+                        dst[0] = xs[0];
+                    } else if (j < head + npair) {
+                        const int o = head + 2 * (j - head);
+                        *reinterpret_cast<double2 *>(dst + o) = make_double2(xs[o], xs[o + 1]);
+                    } else {
+                        dst[nrow - 1] = xs[nrow - 1];
+                    }
+                }
             }
         }
         GTL(e, 3);
@@ -531,19 +566,39 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
     // The RK4 steps run in segments that end at the next recording step or the next
     // change of the held drive sample, so the hot loop carries no record / sample
     // bookkeeping (a latency-bound chain: every issued instruction counts).
-    auto rk4 = [&]() {
-        const V3 k1 = row_rhs(m, coupling(m.x), cin, c);
+    //
+    // The four h_s divisions of a step use rdiv_spec (seed + five DFMA on the
+    // chain instead of __ddiv_rn's ~113 cycles); each one's proof of correct
+    // rounding is folded into `ok` off the chain and checked once per step.
+    // A failed proof (never seen in practice) replays the step from its start
+    // with the library division, so the bits are __ddiv_rn's either way.
+    auto rk4_body = [&](auto spec, bool *ok) {
+        constexpr bool S = decltype(spec)::value;
+        const V3 k1 = row_rhs<S>(m, coupling(m.x), cin, c, ok);
         V3 s = stage_point(m, k1, p.h2);
         publish(s.x);
-        const V3 k2 = row_rhs(s, coupling(s.x), cin, c);
+        const V3 k2 = row_rhs<S>(s, coupling(s.x), cin, c, ok);
         const V3 acc = acc_k2(k1, k2);
         s = stage_point(m, k2, p.h2);
         publish(s.x);
-        const V3 k3 = row_rhs(s, coupling(s.x), cin, c);
+        const V3 k3 = row_rhs<S>(s, coupling(s.x), cin, c, ok);
         s = stage_point(m, k3, p.dt);
         publish(s.x);
-        const V3 k4 = row_rhs(s, coupling(s.x), cin, c);
-        m = rk4_final(m, acc, k3, k4, p.dt6);
+        const V3 k4 = row_rhs<S>(s, coupling(s.x), cin, c, ok);
+        return rk4_final(m, acc, k3, k4, p.dt6);
+    };
+    auto rk4 = [&]() {
+        bool ok = true;
+        const V3 m1 = rk4_body(std::true_type{}, &ok);
+        bool replay;
+        if constexpr (NMAX == 1) replay = !ok;
+        else replay = __any_sync(0xffffffffu, live && !ok);
+        if (replay) {
+            publish(m.x);  // the stage x of the failed attempt are in xsh
+            m = rk4_body(std::false_type{}, nullptr);
+        } else {
+            m = m1;
+        }
         publish(m.x);
     };
     long long step = 0;
@@ -584,6 +639,19 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
         p.m[3 * k] = m.x;
         p.m[3 * k + 1] = m.y;
         p.m[3 * k + 2] = m.z;
+    }
+}
+
+// sto_selftest_div: rdiv_spec and its proof against the library division.
+__global__ void selftest_div_kernel(const double *__restrict__ a, const double *__restrict__ b,
+                                    long long count, double *__restrict__ q, int32_t *__restrict__ ok,
+                                    double *__restrict__ ref) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x) {
+        bool good;
+        q[i] = rdiv_spec(a[i], b[i], good);
+        ok[i] = good ? 1 : 0;
+        ref[i] = rdiv(a[i], b[i]);
     }
 }
 

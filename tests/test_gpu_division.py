@@ -1,0 +1,101 @@
+"""The kernels' speculative division (sto_device.cuh rdiv_spec) against the
+library's IEEE division.
+
+h_s = pref / (1 + lambda * (m . p)) (model.py:250, cpu_jit.py:68) is the one
+division of the RHS; the kernels take it from a short FMA chain whose correct
+rounding is proved per call (`ok`) and replay the RK4 step with __ddiv_rn when a
+proof fails.  So the contract tested here is: ok => bit-equal to __ddiv_rn,
+and ok is (almost) always true on the domain the kernels see.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(a: np.ndarray, b: np.ndarray):
+    from paper_2312_01121_b200 import _native
+
+    da = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+    db = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).cuda()
+    q, ok, ref = _native.selftest_div(da, db)
+    torch.cuda.synchronize()
+    return q.cpu().numpy(), ok.cpu().numpy().astype(bool), ref.cpu().numpy()
+
+
+def _assert_proof_sound(a, b):
+    q, ok, ref = _run(a, b)
+    qb, rb = q.view(np.uint64), ref.view(np.uint64)
+    bad = ok & (qb != rb)
+    assert not bad.any(), (f"{int(bad.sum())} proved quotients differ from __ddiv_rn, e.g. "
+                           f"a={a[bad][0]!r} b={b[bad][0]!r} q={q[bad][0]!r} ref={ref[bad][0]!r}")
+    return q, ok, ref
+
+
+def test_rhs_domain_always_proved(params):
+    """pref / d for d = 1 + lambda*(m.p), |m.p| <= 1.5 (beyond the unit sphere,
+    as a diverging run sees), pref over the physical range: every call proved."""
+    from paper_2312_01121_b200 import derive
+
+    rng = np.random.default_rng(0)
+    cnt = 4_000_000
+    pref = derive(params).h_s_prefactor
+    lam = params.lambda_stt
+    md = rng.uniform(-1.5, 1.5, cnt)
+    d = 1.0 + lam * md
+    a = np.where(rng.random(cnt) < 0.5, pref, pref * rng.uniform(1e-3, 1e3, cnt))
+    q, ok, ref = _assert_proof_sound(a, d)
+    assert ok.all(), f"{int((~ok).sum())} of {cnt} RHS-domain divisions fell back"
+    # and the speculative quotient itself is the IEEE one whenever proved
+    np.testing.assert_array_equal(q.view(np.uint64), ref.view(np.uint64))
+
+
+def test_random_bit_patterns_sound():
+    """Uniform random 64-bit patterns (NaN, inf, zeros, subnormals, every
+    exponent): no proved quotient may differ from __ddiv_rn."""
+    rng = np.random.default_rng(1)
+    cnt = 4_000_000
+    a = rng.integers(0, 2**64, cnt, dtype=np.uint64).view(np.float64)
+    b = rng.integers(0, 2**64, cnt, dtype=np.uint64).view(np.float64)
+    _assert_proof_sound(a, b)
+
+
+def test_wide_normal_range_sound_and_mostly_proved():
+    rng = np.random.default_rng(2)
+    cnt = 4_000_000
+    a = rng.uniform(1, 2, cnt) * np.exp2(rng.integers(-300, 300, cnt)) * rng.choice([-1, 1], cnt)
+    b = rng.uniform(1, 2, cnt) * np.exp2(rng.integers(-150, 150, cnt)) * rng.choice([-1, 1], cnt)
+    _, ok, _ = _assert_proof_sound(a, b)
+    assert ok.mean() > 0.999
+
+
+def test_near_midpoint_quotients_sound():
+    """a chosen so that a/b lies within a few ulps of a rounding midpoint (the
+    hard cases of any division): q0 + rem*y lands next to the boundary, so the
+    proof must reject exactly the wrong ones."""
+    rng = np.random.default_rng(3)
+    cnt = 2_000_000
+    b = rng.uniform(1, 2, cnt)
+    q = rng.uniform(1, 2, cnt)
+    up = np.nextafter(q, np.inf)
+    # a ~ b * (q + up) / 2 in extended precision, rounded to double, then nudged
+    mid = (q.astype(np.longdouble) + up.astype(np.longdouble)) / 2
+    a = (b.astype(np.longdouble) * mid).astype(np.float64)
+    nudge = rng.integers(-3, 4, cnt)
+    a = a + nudge * np.spacing(a)
+    _assert_proof_sound(a, b)
+
+
+def test_power_of_two_quotients_sound():
+    rng = np.random.default_rng(4)
+    cnt = 1_000_000
+    b = rng.uniform(1, 2, cnt)
+    k = rng.integers(-20, 20, cnt)
+    a = b * np.exp2(k)  # exact: quotient 2^k
+    for d in (-2, -1, 0, 1, 2):
+        _assert_proof_sound(a + d * np.spacing(a), b)

@@ -114,6 +114,47 @@ def test_ensemble_divergence_reports_member(sto):
     assert info.value.step == 5 and info.value.oscillator == 0
 
 
+def test_ensemble_stops_at_first_diverged_record(sto):
+    """The run ends at the first recording step with a non-finite state
+    (integrator.py:174-177) instead of integrating NaNs to the horizon: 2e6 RK4
+    steps (~10 s if run out) with a member blowing up at step 1 must return at
+    once.  Members in other half-columns stop there too."""
+    import time
+
+    n, steps = 16, 2_000_000
+    top = sto.Topology.decoupled(n)
+    params = [sto.PhysicalParams()] * 100 + [sto.PhysicalParams(h_appl=1e300)]
+    cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=5)
+    sto.integrate_ensemble(top, params[:4], sto.RunConfig(n=n, steps=10, dt=1e-11))  # warm-up
+    t0 = time.perf_counter()
+    with pytest.raises(sto.IntegrationDivergedError) as info:
+        sto.integrate_ensemble(top, params, cfg)
+    elapsed = time.perf_counter() - t0
+    assert info.value.member == 100 and info.value.step == 5
+    assert elapsed < 2.0, f"diverged ensemble took {elapsed:.2f} s: it did not stop early"
+
+
+def test_ensemble_divergence_earliest_step_across_half_columns(sto):
+    """Two members in different half-columns diverge at different recording
+    steps (per-member drives blow up at different samples): the reported
+    divergence is the earliest step, whichever half-column runs ahead."""
+    n, batch, sps = 16, 160, 5
+    top = sto.Topology(sto.CouplingMatrix.zeros(n), sto.InputWeights(np.ones((n, 1))))
+    params = [sto.PhysicalParams()] * batch
+    series = []
+    for b in range(batch):
+        u = np.zeros((40, 1))
+        if b == 3:
+            u[6:] = 1e300   # diverges in step 31..35 -> recording step 35
+        if b == 130:
+            u[2:] = 1e300   # diverges in step 11..15 -> recording step 15
+        series.append(sto.InputSeries(u, sps))
+    cfg = sto.RunConfig(n=n, steps=200, dt=1e-11, record_stride=5)
+    with pytest.raises(sto.IntegrationDivergedError) as info:
+        sto.integrate_ensemble(top, params, cfg, input_series=series)
+    assert info.value.member == 130 and info.value.step == 15
+
+
 def _rand_top(sto, n, n_in=1, seed=0):
     g = np.random.default_rng(seed)
     w = g.uniform(-1, 1, (n, n)) / np.sqrt(max(n, 3) / 3.0)

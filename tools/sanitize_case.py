@@ -40,7 +40,7 @@ CASES = {
     "reg_single_n100": ("reg", 100, 4, 2, {}),
     "reg_grid_n700": ("reg", 700, 3, 1, {}),
     "single_n60": ("single", 60, 4, 2, {}),
-    "resident_n2000": ("resident", 2000, 2, 1, {}),
+    "resident_n1500": ("resident", 1500, 2, 1, {}),
     "stream_l2_n3000": ("stream", 3000, 2, 1, {}),
     "stream_chunked_n3000": ("stream", 3000, 2, 1, {"STO_CHUNK_COLS": "1024"}),
     "stream_hbm_n3600": ("stream", 3600, 2, 1, {}),
