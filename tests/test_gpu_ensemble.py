@@ -48,6 +48,34 @@ def test_benched_config_members_within_reference_gpu_tolerance(sto, oracle_mod):
     print(f"configs[3] at 1e3 steps: max deviation {worst:.3e} over 8 members")
 
 
+# configs[3] at the benched horizon (1e4 RK4 steps): the reference states no
+# GPU bar beyond 1e3 steps (cli.py:227-233).  Its OWN GPU backend (spinosc
+# TorchBackend: cuBLAS mv order, gpu.py:83-119) deviates from the pinned CPU
+# path by 7.9e-10 (member 0) / 3.7e-10 (member 511) there -- the dynamics
+# amplify any rounding-order difference ~10x per 3e3 steps -- and this DMMA
+# path by 1.1e-9 / 3.9e-10, max 3.4e-9 over 8 members (tools/ens_horizon_bar.py,
+# profiles/r02b_ens_horizon_bar.json).  Bar at 1e4 steps: 1e-8.  (The exact
+# ensemble mode is bit-identical at any horizon.)
+TOL_1E4 = 1e-8
+
+
+def test_benched_horizon_members_within_stated_bar(sto, oracle_mod):
+    n, batch, steps = 1000, 512, 10_000
+    top = sto.build_topology(n, seed=0)
+    params = _sweep(sto, batch)
+    cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=1000)
+    ens = sto.integrate_ensemble(top, params, cfg)
+    worst = 0.0
+    for b in (0, 146, 511):
+        want, _ = oracle_mod.integrate(top.coupling.entries, top.input_weights.entries,
+                                       sto.kernel_scalars(params[b]), sto.initial_state(n),
+                                       np.zeros((1, 1)), 1, 1e-11, steps, 1000)
+        dev = float(np.abs(ens.states[:, b] - want).max())
+        worst = max(worst, dev)
+        assert dev <= TOL_1E4, f"member {b}: {dev:.3e} at 1e4 steps"
+    print(f"configs[3] at 1e4 steps: max deviation {worst:.3e} over 3 members")
+
+
 def _sweep(sto, batch):
     return [sto.PhysicalParams(current=c) for c in np.linspace(2.0e-3, 3.0e-3, batch)]
 

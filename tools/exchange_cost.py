@@ -3,7 +3,8 @@ one GPU: the same MULTI grid kernel and protocol as the
 multi-GPU path (each CTA pushes its x slice into every rank's receive buffer,
 local counter barrier, epoch flags with st.release.sys, fence.acq_rel.sys),
 only the peer buffers are local.  world = 1 is the unsharded grid kernel
-(grid barrier, no peer stores).  Prints one JSON line per (n, world):
+(grid barrier, no peer stores).  Every plan streams W (FORCE_STREAM), so the
+CTA-level work is the same and the difference is the exchange.  Prints one JSON line per (n, world):
 microseconds per RK stage and the difference to world = 1.
 
     python tools/exchange_cost.py [n ...]
@@ -56,7 +57,7 @@ def main():
             m = m0.clone()
             if world == 1:
                 plan = _native.Plan(top.coupling.entries, top.input_weights.entries, consts,
-                                    device=0, flags=_native.NO_CLUSTER | _native.NO_REG)
+                                    device=0, flags=_native.FORCE_STREAM)
                 kind = plan.info["kernel_name"]
 
                 def run():
@@ -64,7 +65,7 @@ def main():
                     plan.integrate_dev(m, u, 1, 1e-11, steps, steps, None)
                 plans = [plan]
             else:
-                plans = [_shard_plan(top, consts, b, c, world, r, 0)
+                plans = [_shard_plan(top, consts, b, c, world, r, 0, _native.FORCE_STREAM)
                          for r, (b, c) in enumerate(shard_rows(n, world))]
                 _native.connect_local(plans)
                 kind = "MULTI"

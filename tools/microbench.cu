@@ -30,6 +30,16 @@ __global__ void chain_kernel(int which, int iters, double seed, double *out, lon
         case 4:
             for (int i = 0; i < iters; ++i) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, 1));
             break;
+        case 5: {  // speculative division (sto_device.cuh rdiv_spec): chain latency, proof off-chain
+            bool okall = true;
+            for (int i = 0; i < iters; ++i) {
+                bool ok;
+                x = rdiv_spec(y, x, ok);
+                okall &= ok;
+            }
+            if (!okall) x = -x;
+            break;
+        }
     }
     long long t1 = clock64();
     if (threadIdx.x == 0) {
@@ -70,6 +80,45 @@ __global__ void rk4_chain(int steps, Consts c, double dt, double *out, long long
     }
     long long t1 = clock64();
     out[0] = m.x + m.y + m.z;
+    cyc[0] = t1 - t0;
+}
+
+// the same chain with the tiny kernel's speculative division (rdiv_spec, one
+// proof check per step, replay with __ddiv_rn on a failed proof)
+__global__ void rk4_chain_spec(int steps, Consts c, double dt, double *out, long long *cyc) {
+    V3 m{0.0174497, 0.000304586, 0.999847695};
+    const double h2 = dt * 0.5, dt6 = dt / 6.0, w = 0.0, cin = 0.0;
+    long long t0 = clock64();
+    int replays = 0;
+    for (int s = 0; s < steps; ++s) {
+        bool ok = true;
+        const V3 k1 = row_rhs<true>(m, rmul(w, m.x), cin, c, &ok);
+        V3 st = stage_point(m, k1, h2);
+        const V3 k2 = row_rhs<true>(st, rmul(w, st.x), cin, c, &ok);
+        const V3 acc = acc_k2(k1, k2);
+        st = stage_point(m, k2, h2);
+        const V3 k3 = row_rhs<true>(st, rmul(w, st.x), cin, c, &ok);
+        st = stage_point(m, k3, dt);
+        const V3 k4 = row_rhs<true>(st, rmul(w, st.x), cin, c, &ok);
+        const V3 mn = rk4_final(m, acc, k3, k4, dt6);
+        if (!ok) {
+            ++replays;
+            const V3 j1 = row_rhs(m, rmul(w, m.x), cin, c);
+            V3 t = stage_point(m, j1, h2);
+            const V3 j2 = row_rhs(t, rmul(w, t.x), cin, c);
+            const V3 a2 = acc_k2(j1, j2);
+            t = stage_point(m, j2, h2);
+            const V3 j3 = row_rhs(t, rmul(w, t.x), cin, c);
+            t = stage_point(m, j3, dt);
+            const V3 j4 = row_rhs(t, rmul(w, t.x), cin, c);
+            m = rk4_final(m, a2, j3, j4, dt6);
+        } else {
+            m = mn;
+        }
+    }
+    long long t1 = clock64();
+    out[0] = m.x + m.y + m.z;
+    out[1] = replays;
     cyc[0] = t1 - t0;
 }
 
@@ -262,9 +311,9 @@ int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     long long h;
-    const char *names[] = {"dadd", "dmul", "ddiv", "shfl_f64", "shfl_f64+dadd"};
+    const char *names[] = {"dadd", "dmul", "ddiv", "shfl_f64", "shfl_f64+dadd", "ddiv_spec"};
     printf("{\"sm_count\": %d, \"clock_khz\": %d", sms, clk_khz);
-    for (int w = 0; w < 5; ++w) {
+    for (int w = 0; w < 6; ++w) {
         const int iters = 100000;
         chain_kernel<<<1, 32>>>(w, iters, 1.5, out, cyc);
         chain_kernel<<<1, 32>>>(w, iters, 1.5, out, cyc);
@@ -288,6 +337,17 @@ int main() {
     cudaEventElapsedTime(&ms, a, b);
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     printf(", \"rk4_step_cyc\": %.1f, \"rk4_step_ns\": %.1f", (double)h / 100000, ms * 1e6 / 100000);
+    rk4_chain_spec<<<1, 1>>>(100000, c, 1e-11, out, cyc);
+    cudaEventRecord(a);
+    rk4_chain_spec<<<1, 1>>>(100000, c, 1e-11, out, cyc);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    double hr[2];
+    cudaMemcpy(hr, out, 16, cudaMemcpyDeviceToHost);
+    printf(", \"rk4_step_spec_cyc\": %.1f, \"rk4_step_spec_ns\": %.1f, \"rk4_spec_replays\": %.0f",
+           (double)h / 100000, ms * 1e6 / 100000, hr[1]);
 
     unsigned long long *bar;
     cudaMalloc(&bar, 64);
