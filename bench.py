@@ -61,12 +61,19 @@ WORKLOADS["n100_rec1"] = (100, 10_000, "configs[0] with record_stride=1: N=100, 
                           "drive, every state recorded (24 MB of states per run)", True)
 WORKLOADS["n1e4_rec10"] = (10_000, 1000, "configs[4] with record_stride=10: N=1e4, 1e3 RK4 steps, "
                            "every 10th state recorded (24 MB of states per run)", False)
+WORKLOADS["ens512_exact"] = (1000, 10_000, "configs[3] bit-exact mode: N=1000 x B=512 ensemble (current "
+                             "sweep 2.0-3.0 mA), 1e4 RK4 steps, pinned-tree coupling on the FP64 CUDA cores",
+                             False)
 RECORD_STRIDE = {"n100_rec1": 1, "n1e4_rec10": 10}
-ENSEMBLE_BATCH = {"ens512": 512}
+ENSEMBLE_BATCH = {"ens512": 512, "ens512_exact": 512}
+EXACT_ENSEMBLE = ("ens512_exact",)
 SHARDED_WORKLOADS = ("n1e4", "n4e4", "n1e4_rec10")  # row-sharded over GPUs when --gpus > 1
 # FP64 peaks measured on this pool's B200 (tools/fp64_peak.cu; MEASURED_PEAKS.json has
 # none): DMMA m8n8k4 37.1 TFLOP/s, DFMA 34.0, cuBLAS DGEMM 8192^3 35.5.
 FP64_TENSOR_PEAK_TFLOPS = 37.1
+# the bit-exact mode issues every product and sum separately (no FMA: the pinned
+# order), so its ceiling is the FP64 pipe's instruction rate = half the DFMA flops
+FP64_MULADD_PEAK_TFLOPS = 34.0 / 2
 DT = 1e-11
 
 
@@ -75,7 +82,13 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-RK4_CHAIN_CYCLES = 1125  # profiles/r01_microbench.json "rk4_step_cyc"
+# Dependent fp64 chain of one RK4 step in the pinned order (sto_device.cuh): 15
+# dependent DMUL/DADD between two h_s divisions in stages 1-3 (m.p, 1 + lam*md,
+# then h_s*q_z -> b_z -> a_y -> e_x -> dm/dt -> stage point) and 17 around the
+# RK4 combination, i.e. 62 x 8.4 cycles, plus 4 speculative divisions at 74.25
+# cycles (tools/microbench.cu, profiles/r02c_microbench.json: dadd 8.44, dmul
+# 8.38, ddiv_spec 74.25; __ddiv_rn was 113.5) = 818 cycles.
+RK4_CHAIN_CYCLES = 62 * 8.4 + 4 * 74.25
 
 
 def measured_peaks() -> dict:
@@ -297,6 +310,7 @@ def run_ours_ensemble(args, rank, world, local_rank):
     if args.rk4_steps:
         steps = args.rk4_steps
     batch_total = ENSEMBLE_BATCH[name]
+    exact = name in EXACT_ENSEMBLE
     currents = np.linspace(2.0e-3, 3.0e-3, batch_total)
     from paper_2312_01121_b200.sharding import shard_members
 
@@ -320,7 +334,8 @@ def run_ours_ensemble(args, rank, world, local_rank):
 
     def one_run():
         m_d.copy_(m0)
-        backend._plan.integrate_ensemble_dev(m_d, c_d, s_d, 1, 0, DT, steps, stride, states_d)
+        backend._plan.integrate_ensemble_dev(m_d, c_d, s_d, 1, 0, DT, steps, stride, states_d,
+                                             exact=exact)
 
     for _ in range(args.warmup):
         one_run()
@@ -348,11 +363,12 @@ def run_ours_ensemble(args, rank, world, local_rank):
     # batch-sharded integrate_ensemble(group=) returns every member on every rank
     cfg = sto.RunConfig(n=n, steps=steps, dt=DT, record_stride=stride, gpu_device=dev)
     group = "world" if dist else None
-    sto.integrate_ensemble(top, params_all, cfg, backend=backend, group=group)
+    sto.integrate_ensemble(top, params_all, cfg, backend=backend, group=group, exact=exact)
     t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 2))
     for _ in range(e2e_steps):
-        ens = sto.integrate_ensemble(top, params_all, cfg, backend=backend, group=group)
+        ens = sto.integrate_ensemble(top, params_all, cfg, backend=backend, group=group,
+                                     exact=exact)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if dist:
         t = torch.tensor([e2e_s], device="cuda")
@@ -378,17 +394,26 @@ def run_ours_ensemble(args, rank, world, local_rank):
             "config": {"workload": desc, "n": n, "batch": batch_total, "rk4_steps_per_run": steps,
                        "record_stride": stride, "dt": DT,
                        "parallelism": f"batch-sharded x{world}" if world > 1 else "1 GPU",
-                       "kernel": "ens_rk4_kernel (DMMA m8n8k4 f64)",
-                       "l2": "W 8 MB + stage x 8 MB L2-resident (fragment order), RK state in TMEM; one launch per run"},
+                       "kernel": ("ens_exact_kernel (pinned tree, DMUL+DADD, bit-exact per member)" if exact
+                                  else "ens_rk4_kernel (DMMA m8n8k4 f64)"),
+                       "l2": ("W 8 MB + stage x 8 MB + RK state planes L2-resident; one launch per run" if exact
+                              else "W 8 MB + stage x 8 MB L2-resident (fragment order), RK state in TMEM; "
+                                   "one launch per run")},
             "e2e": {"value": batch_total * n * steps / e2e_s, "unit": "osc-steps/s",
                     "h2d_bytes_per_step": 8 * (n * n + n + batch * 3 * n + batch * 11),
                     "d2h_bytes_per_step": 8 * ens.states.size // world},
             "gpu_launches": 2 * args.steps,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_TENSOR_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / FP64_TENSOR_PEAK_TFLOPS,
-                         "traffic": traffic_per_launch("ens512", steps),
-                         "peak_source": "measured here: DMMA f64 microbenchmark (tools/fp64_peak.cu)",
-                         "kernel": "ens_rk4_kernel"},
+            "roofline": ({"bound": "fp64", "achieved": achieved, "peak": FP64_MULADD_PEAK_TFLOPS,
+                          "unit": "TFLOP/s", "frac": achieved / FP64_MULADD_PEAK_TFLOPS,
+                          "traffic": None,
+                          "peak_source": "FP64 CUDA-core mul/add issue rate: half the measured DFMA "
+                                         "34.0 TFLOP/s (tools/fp64_peak.cu); the pinned order forbids FMA",
+                          "kernel": "ens_exact_kernel"} if exact else
+                         {"bound": "tensor", "achieved": achieved, "peak": FP64_TENSOR_PEAK_TFLOPS,
+                          "unit": "TFLOP/s", "frac": achieved / FP64_TENSOR_PEAK_TFLOPS,
+                          "traffic": traffic_per_launch("ens512", steps),
+                          "peak_source": "measured here: DMMA f64 microbenchmark (tools/fp64_peak.cu)",
+                          "kernel": "ens_rk4_kernel"}),
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }
@@ -548,15 +573,16 @@ def run_ours(args, rank, world, local_rank):
                                 "(SURVEY 8(d)); DRAM traffic is %.2g of the algorithmic bytes" % share)
     if n < 1000:
         # W is a few KB: no HBM/tensor roofline applies.  The bound is the dependent
-        # fp64 chain of one RK4 step (4 RHS evaluations, DDIV included): 1125 cycles
-        # measured by tools/microbench.cu (profiles/r01_microbench.json).
+        # fp64 chain of one RK4 step (4 RHS evaluations, divisions included):
+        # RK4_CHAIN_CYCLES, from the latencies tools/microbench.cu measures.
         clk = clocks.summary().get("sm_mhz") or 1965.0
         peak_steps = clk * 1e6 / RK4_CHAIN_CYCLES
         got = steps / kernel_s
         roofline = {"bound": "latency", "achieved": got, "peak": peak_steps, "unit": "RK4 steps/s",
                     "frac": got / peak_steps, "traffic": traffic_per_launch(name, steps),
-                    "peak_source": f"measured dependent-chain bound ({RK4_CHAIN_CYCLES} cycles per RK4 "
-                                   f"step at {clk:.0f} MHz, tools/microbench.cu)",
+                    "peak_source": f"dependent-chain bound ({RK4_CHAIN_CYCLES:.0f} cycles per RK4 step = 62 "
+                                   f"dependent DMUL/DADD + 4 speculative divisions, latencies measured "
+                                   f"by tools/microbench.cu; at {clk:.0f} MHz)",
                     "kernel": kname}
 
     # ----------------------------------------------------- cpu baseline ----

@@ -163,6 +163,12 @@ typedef struct {
 
 STO_API int sto_integrate_ensemble(sto_plan *plan, const sto_ensemble_run *run,
                                    sto_status *status, void *stream);
+/* The same run, bit-exact: every member's states equal integrate() / the
+ * reference's pinned CPU path with that member's parameters and drive, at any
+ * horizon (pinned adjacent-pairs tree on the CUDA cores, pinned RHS and RK4
+ * order; sto_ensemble_exact.cuh).  n <= 8160.  Same arguments and status. */
+STO_API int sto_integrate_ensemble_exact(sto_plan *plan, const sto_ensemble_run *run,
+                                         sto_status *status, void *stream);
 
 /* Row-sharded multi-GPU (one process per GPU).  Each rank exports the IPC
  * handle of its exchange buffer (64 bytes, cudaIpcMemHandle_t), the caller

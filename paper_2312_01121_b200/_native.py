@@ -85,6 +85,8 @@ SIGNATURES = {
                                               ctypes.POINTER(Status), ctypes.c_void_p]),
     "sto_plan_last_status": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Status),
                                             ctypes.c_void_p]),
+    "sto_integrate_ensemble_exact": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(EnsembleRun),
+                                                    ctypes.POINTER(Status), ctypes.c_void_p]),
     "sto_plan_exchange_handle": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
                                                 ctypes.c_int64]),
     "sto_plan_connect": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]),
@@ -299,8 +301,10 @@ class Plan:
 
     def integrate_ensemble_dev(self, m, consts, samples, steps_per_sample: int,
                                sample_member_stride: int, dt: float, steps: int, stride: int,
-                               states) -> Status:
-        """Batched members (m: (B, n, 3), consts: (B, 11)); synchronous status."""
+                               states, exact: bool = False) -> Status:
+        """Batched members (m: (B, n, 3), consts: (B, 11)); synchronous status.
+        exact: the bit-exact CUDA-core path (sto_integrate_ensemble_exact) instead
+        of the DMMA tensor-core path."""
         run = EnsembleRun(batch=m.shape[0], consts=consts.data_ptr(), m=m.data_ptr(),
                           samples=samples.data_ptr(), n_samples=samples.shape[-2],
                           steps_per_sample=int(steps_per_sample),
@@ -308,8 +312,8 @@ class Plan:
                           steps=int(steps), record_stride=int(stride),
                           states=states.data_ptr() if states is not None else None)
         st = Status()
-        rc = lib().sto_integrate_ensemble(self._h, ctypes.byref(run), ctypes.byref(st),
-                                          _stream_ptr(self.device))
+        fn = lib().sto_integrate_ensemble_exact if exact else lib().sto_integrate_ensemble
+        rc = fn(self._h, ctypes.byref(run), ctypes.byref(st), _stream_ptr(self.device))
         if rc == STO_E_DIVERGED:
             from .errors import IntegrationDivergedError
 

@@ -144,10 +144,11 @@ class B200Backend:
 
     def integrate_ensemble_run(self, consts: np.ndarray, samples: np.ndarray,
                                steps_per_sample: int, dt: float, steps: int, stride: int,
-                               m0: np.ndarray) -> np.ndarray:
+                               m0: np.ndarray, exact: bool = False) -> np.ndarray:
         """B members sharing W/W_in: consts (B, 11), m0 (B, n, 3) updated in place,
         samples (n_samples, n_in) shared or (B, n_samples, n_in) per member.
-        Returns states (n_records, B, n, 3)."""
+        Returns states (n_records, B, n, 3).  exact=True: bit-exact CUDA-core
+        path (each member == integrate() with its parameters) instead of DMMA."""
         t = self._torch
         consts = np.ascontiguousarray(consts, dtype=np.float64)
         batch = consts.shape[0]
@@ -169,7 +170,7 @@ class B200Backend:
             start, stop = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
             start.record()
             self._plan.integrate_ensemble_dev(m_d, c_d, s_d, steps_per_sample, stride_m, dt,
-                                              steps, stride, states_d)
+                                              steps, stride, states_d, exact=exact)
             stop.record()
             stop.synchronize()
             self.last_kernel_seconds = start.elapsed_time(stop) / 1e3

@@ -16,6 +16,7 @@
 #include "sto_reg_kernel.cuh"
 #include "sto_cluster_kernel.cuh"
 #include "sto_ensemble_kernel.cuh"
+#include "sto_ensemble_exact.cuh"
 #include "sto_build.cuh"
 
 using namespace sto;
@@ -140,6 +141,18 @@ __global__ void ens_layout_kernel(const double *__restrict__ src, double *__rest
     }
 }
 
+// Exact-ensemble W: row-major np x kp, logical columns, -0.0 outside n x n
+// (sto_ensemble_exact.cuh: the padding identity of the pinned tree).
+__global__ void ex_layout_kernel(const double *__restrict__ src, double *__restrict__ dst, int n, int np,
+                                 int kp, ColSched cs) {
+    const long long total = (long long)np * kp;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(i / kp), col = (int)(i - (long long)row * kp);
+        dst[i] = (row < n && col < n) ? src[(long long)row * cs.ldw + col_perm(cs, col)] : -0.0;
+    }
+}
+
 __global__ void reset_status_kernel(StatusDev *st, unsigned long long *bar, unsigned *flags) {
     for (int i = threadIdx.x; i < kMaxFlags; i += blockDim.x) flags[i] = 0u;
     if (threadIdx.x == 0) {
@@ -253,6 +266,11 @@ struct sto_plan {
     double *ens_x = nullptr, *ens_st = nullptr;
     size_t ens_bp = 0;                 // member capacity of ens_x / ens_st
     unsigned long long *ens_bar = nullptr;
+    // exact (CUDA-core, pinned-tree) ensemble resources
+    double *ex_w = nullptr;            // ex_np x ex_kp row-major, -0.0 padded
+    double *ex_x = nullptr, *ex_st = nullptr;
+    size_t ex_bp = 0;                  // member capacity of ex_x / ex_st
+    unsigned long long *ex_bar = nullptr;
 };
 
 namespace {
@@ -752,6 +770,10 @@ void sto_plan_destroy(sto_plan *P) {
     cudaFree(P->ens_x);
     cudaFree(P->ens_st);
     cudaFree(P->ens_bar);
+    cudaFree(P->ex_w);
+    cudaFree(P->ex_x);
+    cudaFree(P->ex_st);
+    cudaFree(P->ex_bar);
     cudaFree(P->status);
     delete P;
 }
@@ -990,6 +1012,104 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
         STO_CUDA(cudaMemsetAsync(P->ens_bar, 0, sizeof(unsigned long long) * 32 * 1024, s));
         const int rc = launch_ens_u(U, e, n_rt * ncols, s);
         if (rc) return rc;
+    }
+    if (!status) return STO_OK;
+    StatusDev h{};
+    STO_CUDA(cudaMemcpyAsync(&h, P->status, sizeof(h), cudaMemcpyDeviceToHost, s));
+    STO_CUDA(cudaStreamSynchronize(s));
+    status->diverged = h.flag;
+    status->reserved = h.flag ? (int32_t)((h.key >> 20) & 0xfffff) : -1;  // member
+    status->oscillator = h.flag ? (h.key & 0xfffff) : -1;
+    status->step = h.flag ? (h.key >> 40) : -1;
+    if (h.flag)
+        return fail(STO_E_DIVERGED, "member " + std::to_string(status->reserved) +
+                                        ": non-finite state for oscillator " +
+                                        std::to_string(status->oscillator) + " at step " +
+                                        std::to_string(status->step));
+    return STO_OK;
+}
+
+int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_status *status,
+                                 void *stream) {
+    if (!P || !r) return fail(STO_E_PARAM, "null plan or run");
+    if (r->batch < 1 || !r->consts || !r->m || !r->samples || r->n_samples < 1 ||
+        r->steps_per_sample < 1 || r->steps < 1 || r->record_stride < 1 || !(r->dt > 0.0) ||
+        r->batch >= (1 << 20) || P->n >= (1 << 20) || r->steps >= (1LL << 23))
+        return fail(STO_E_PARAM, "bad ensemble run descriptor");
+    if (P->world > 1) return fail(STO_E_PARAM, "ensemble needs an unsharded plan");
+    const int kp = ((P->n + kExKC - 1) / kExKC) * kExKC;
+    const int n_chunks = kp / kExKC;
+    int levels = 1;
+    while ((1 << levels) <= n_chunks) ++levels;  // bit length of n_chunks
+    if (levels > kExMaxLevels) return fail(STO_E_PARAM, "exact ensemble supports n <= 8160");
+    STO_CUDA(cudaSetDevice(P->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int np = ((P->n + kExTR - 1) / kExTR) * kExTR;
+    const int n_rt = np / kExTR;
+    const int total_ct = (int)((r->batch + kExTB - 1) / kExTB);
+    const int grid = std::min(P->sm_count, n_rt * total_ct);
+    // member tiles per launch: at most kExMaxTiles tiles per CTA
+    int ct_per_launch = std::max(1, std::min(total_ct, (kExMaxTiles * grid) / n_rt));
+    if (const char *ev = getenv("STO_EX_CT_PER_LAUNCH"))  // test knob: force several launches
+        ct_per_launch = std::max(1, std::min(ct_per_launch, atoi(ev)));
+    const size_t bp = (size_t)ct_per_launch * kExTB;
+    if (!P->ex_w) {
+        STO_CUDA(cudaMalloc(&P->ex_w, sizeof(double) * (size_t)np * kp));
+        STO_CUDA(cudaMalloc(&P->ex_bar, sizeof(unsigned long long) * 32 * 4096));
+        ex_layout_kernel<<<1184, 256, 0, s>>>(P->L.w, P->ex_w, P->n, np, kp, P->L.cs);
+        STO_CUDA(cudaGetLastError());
+    }
+    if (P->ex_bp < bp) {
+        cudaFree(P->ex_x);
+        cudaFree(P->ex_st);
+        P->ex_x = P->ex_st = nullptr;
+        STO_CUDA(cudaMalloc(&P->ex_x, sizeof(double) * 2 * kp * bp));
+        STO_CUDA(cudaMalloc(&P->ex_st, sizeof(double) * kExPlanes * np * bp));
+        P->ex_bp = bp;
+    }
+    if (ct_per_launch > 4096) return fail(STO_E_PARAM, "too many member tiles");
+    const size_t smem = ex_smem_bytes(levels);
+    STO_CUDA(cudaFuncSetAttribute(ens_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    reset_status_kernel<<<1, 256, 0, s>>>(P->status, P->bar, P->flags);
+    STO_CUDA(cudaGetLastError());
+    for (int c0 = 0; c0 < total_ct; c0 += ct_per_launch) {
+        const int nct = std::min(ct_per_launch, total_ct - c0);
+        ExParams e{};
+        e.n = P->n;
+        e.np = np;
+        e.kp = kp;
+        e.n_rt = n_rt;
+        e.n_ct = nct;
+        e.member0 = c0 * kExTB;
+        e.batch = (int)std::min<int64_t>((int64_t)nct * kExTB, r->batch - e.member0);
+        e.batch_total = (int)r->batch;
+        e.bp = (int)bp;
+        e.n_in = P->n_in;
+        e.levels = levels;
+        e.w = P->ex_w;
+        e.w_in = P->w_in;
+        e.consts = r->consts;
+        e.m = r->m;
+        e.samples = r->samples;
+        e.sample_member_stride = r->sample_member_stride;
+        e.n_samples = r->n_samples;
+        e.sps = r->steps_per_sample;
+        e.dt = r->dt;
+        e.h2 = r->dt * 0.5;
+        e.dt6 = r->dt / 6.0;
+        e.steps = r->steps;
+        e.stride = r->record_stride;
+        e.n_records = sto_n_records(r->steps, r->record_stride);
+        e.states = r->states;
+        e.x = P->ex_x;
+        e.st = P->ex_st;
+        e.bar = P->ex_bar;
+        e.status = P->status;
+        STO_CUDA(cudaMemsetAsync(P->ex_x, 0, sizeof(double) * 2 * kp * bp, s));
+        STO_CUDA(cudaMemsetAsync(P->ex_bar, 0, sizeof(unsigned long long) * 32 * nct, s));
+        const int g = std::min(grid, n_rt * nct);
+        void *args[] = {(void *)&e};
+        STO_CUDA(cudaLaunchCooperativeKernel((void *)ens_exact_kernel, dim3(g), dim3(kExThreads), args, smem, s));
     }
     if (!status) return STO_OK;
     StatusDev h{};

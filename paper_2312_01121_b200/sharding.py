@@ -165,7 +165,7 @@ def shard_members(batch: int, world: int, rank: int) -> np.ndarray:
 
 
 def integrate_ensemble_sharded(backend, consts: np.ndarray, samples: np.ndarray,
-                               steps_per_sample: int, config, group) -> np.ndarray:
+                               steps_per_sample: int, config, group, exact: bool = False) -> np.ndarray:
     """Batch-sharded ensemble: this rank's members on its own
     GPU, then one all-gather of the recorded grids.  consts (B, 11) and
     samples ([B,] n_samples, n_in) describe the WHOLE batch; returns the
@@ -187,7 +187,8 @@ def integrate_ensemble_sharded(backend, consts: np.ndarray, samples: np.ndarray,
     states = None
     try:
         states = backend.integrate_ensemble_run(consts[mine], samples_mine, steps_per_sample,
-                                                config.dt, config.steps, config.record_stride, m)
+                                                config.dt, config.steps, config.record_stride, m,
+                                                exact=exact)
         status = (RUN_OK, 0, 0)
     except IntegrationDivergedError as exc:
         # step, then global member, then oscillator: packed so min() keeps that order

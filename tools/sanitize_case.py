@@ -48,6 +48,8 @@ CASES = {
     "multi_w4_n1500_chunked": ("multi4", 1500, 2, 1, {"STO_CHUNK_COLS": "512"}),
     "ensemble_u1": ("ens", 200, 3, 1, {"STO_ENS_U": "1"}),
     "ensemble_u7": ("ens", 200, 3, 1, {"STO_ENS_U": "7"}),
+    "ensemble_exact": ("ensx", 200, 3, 1, {}),
+    "ensemble_exact_2launch": ("ensx", 100, 2, 1, {"STO_EX_CT_PER_LAUNCH": "1"}),
     "derivative_k0": ("deriv", 900, 0, 0, {}),
     "device_build": ("build", 300, 0, 0, {}),
 }
@@ -85,15 +87,18 @@ def main(name: str) -> None:
         got = top_d.coupling.entries
         got = got.cpu().numpy() if hasattr(got, "cpu") else np.asarray(got)
         assert np.allclose(got, top_h.coupling.entries, rtol=1e-12, atol=0)
-    elif fam == "ens":
+    elif fam in ("ens", "ensx"):
         currents = np.linspace(2.0e-3, 3.0e-3, 70)
         params = [sto.PhysicalParams(current=float(c)) for c in currents]
         cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=stride)
-        ens = sto.integrate_ensemble(top, params, cfg)
+        ens = sto.integrate_ensemble(top, params, cfg, exact=fam == "ensx")
         for b in (0, 33, 69):
             want, _ = oracle.integrate(w, w_in, sto.kernel_scalars(params[b]), m0, np.zeros((1, 1)),
                                        1, 1e-11, steps, stride)
-            assert np.abs(ens.states[:, b] - want).max() <= 1e-12
+            if fam == "ensx":
+                assert np.array_equal(ens.states[:, b].view(np.uint64), want.view(np.uint64))
+            else:
+                assert np.abs(ens.states[:, b] - want).max() <= 1e-12
     elif fam.startswith("multi"):
         from paper_2312_01121_b200.sharding import integrate_logical
 
