@@ -1029,6 +1029,26 @@ int sto_integrate_ensemble(sto_plan *P, const sto_ensemble_run *r, sto_status *s
     return STO_OK;
 }
 
+}  // extern "C"
+
+namespace {
+template <int BV>
+const void *ex_kernel_bv(int u) {
+    switch (u) {
+        case 1: return (const void *)ens_exact_kernel<1, BV>;
+        case 2: return (const void *)ens_exact_kernel<2, BV>;
+        case 3: return (const void *)ens_exact_kernel<3, BV>;
+        case 4: return (const void *)ens_exact_kernel<4, BV>;
+        case 5: return (const void *)ens_exact_kernel<5, BV>;
+        case 6: return (const void *)ens_exact_kernel<6, BV>;
+        default: return (const void *)ens_exact_kernel<7, BV>;
+    }
+}
+const void *ex_kernel_of(int u, int bv) { return bv == 2 ? ex_kernel_bv<2>(u) : ex_kernel_bv<1>(u); }
+}  // namespace
+
+extern "C" {
+
 int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_status *status,
                                  void *stream) {
     if (!P || !r) return fail(STO_E_PARAM, "null plan or run");
@@ -1038,25 +1058,47 @@ int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_sta
         return fail(STO_E_PARAM, "bad ensemble run descriptor");
     if (P->world > 1) return fail(STO_E_PARAM, "ensemble needs an unsharded plan");
     const int kp = ((P->n + kExKC - 1) / kExKC) * kExKC;
-    const int n_chunks = kp / kExKC;
+    const int n_leaves = (kp / kExKC + 1) / 2;  // 64-column leaves
     int levels = 1;
-    while ((1 << levels) <= n_chunks) ++levels;  // bit length of n_chunks
-    if (levels > kExMaxLevels) return fail(STO_E_PARAM, "exact ensemble supports n <= 8160");
+    while ((1 << levels) <= n_leaves) ++levels;  // bit length of the leaf count
+    if (levels > kExMaxLevels) return fail(STO_E_PARAM, "exact ensemble supports n <= 16320");
     STO_CUDA(cudaSetDevice(P->device));
     cudaStream_t s = (cudaStream_t)stream;
-    const int np = ((P->n + kExTR - 1) / kExTR) * kExTR;
-    const int n_rt = np / kExTR;
+    // Tile = 8U oscillators x 64 members, one CTA per SM, several tiles per CTA:
+    // minimise the per-CTA work U * ceil(tiles / grid) (ties -> larger U), among
+    // the U whose leaf stack fits shared memory.
+    const int nu = (P->n + 7) / 8;
     const int total_ct = (int)((r->batch + kExTB - 1) / kExTB);
+    int U = 0;
+    long long best = 0;
+    for (int u = 1; u <= kExMaxU; ++u) {
+        if (ex_smem_bytes(u, levels) > kExSmemBudget) continue;
+        const long long tiles = (long long)((nu + u - 1) / u) * total_ct;
+        const long long cost = (long long)u * ((tiles + P->sm_count - 1) / P->sm_count);
+        if (!U || cost <= best) {
+            U = u;
+            best = cost;
+        }
+    }
+    if (!U) return fail(STO_E_PARAM, "exact ensemble: no tile fits shared memory");
+    if (const char *ev = getenv("STO_EX_U")) {  // test knob: force a tile height
+        const int u = atoi(ev);
+        if (u >= 1 && u <= kExMaxU && ex_smem_bytes(u, levels) <= kExSmemBudget) U = u;
+    }
+    const int TR = 8 * U;
+    const int n_rt = (P->n + TR - 1) / TR;
+    const int np_alloc = nu * 8 + 8 * kExMaxU;  // any n_rt * TR fits
     const int grid = std::min(P->sm_count, n_rt * total_ct);
     // member tiles per launch: at most kExMaxTiles tiles per CTA
     int ct_per_launch = std::max(1, std::min(total_ct, (kExMaxTiles * grid) / n_rt));
     if (const char *ev = getenv("STO_EX_CT_PER_LAUNCH"))  // test knob: force several launches
         ct_per_launch = std::max(1, std::min(ct_per_launch, atoi(ev)));
+    if (ct_per_launch > 4096) return fail(STO_E_PARAM, "too many member tiles");
     const size_t bp = (size_t)ct_per_launch * kExTB;
     if (!P->ex_w) {
-        STO_CUDA(cudaMalloc(&P->ex_w, sizeof(double) * (size_t)np * kp));
+        STO_CUDA(cudaMalloc(&P->ex_w, sizeof(double) * (size_t)np_alloc * kp));
         STO_CUDA(cudaMalloc(&P->ex_bar, sizeof(unsigned long long) * 32 * 4096));
-        ex_layout_kernel<<<1184, 256, 0, s>>>(P->L.w, P->ex_w, P->n, np, kp, P->L.cs);
+        ex_layout_kernel<<<1184, 256, 0, s>>>(P->L.w, P->ex_w, P->n, np_alloc, kp, P->L.cs);
         STO_CUDA(cudaGetLastError());
     }
     if (P->ex_bp < bp) {
@@ -1064,19 +1106,22 @@ int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_sta
         cudaFree(P->ex_st);
         P->ex_x = P->ex_st = nullptr;
         STO_CUDA(cudaMalloc(&P->ex_x, sizeof(double) * 2 * kp * bp));
-        STO_CUDA(cudaMalloc(&P->ex_st, sizeof(double) * kExPlanes * np * bp));
+        STO_CUDA(cudaMalloc(&P->ex_st, sizeof(double) * kExPlanes * np_alloc * bp));
         P->ex_bp = bp;
     }
-    if (ct_per_launch > 4096) return fail(STO_E_PARAM, "too many member tiles");
-    const size_t smem = ex_smem_bytes(levels);
-    STO_CUDA(cudaFuncSetAttribute(ens_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t smem = ex_smem_bytes(U, levels);
+    // members per thread: 1 (16 warps, more latency hiding) or 2 (8 warps)
+    int BV = kExDefaultBV;
+    if (const char *ev = getenv("STO_EX_BV")) BV = atoi(ev) == 2 ? 2 : 1;
+    const void *fn = ex_kernel_of(U, BV);
+    STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     reset_status_kernel<<<1, 256, 0, s>>>(P->status, P->bar, P->flags);
     STO_CUDA(cudaGetLastError());
     for (int c0 = 0; c0 < total_ct; c0 += ct_per_launch) {
         const int nct = std::min(ct_per_launch, total_ct - c0);
         ExParams e{};
         e.n = P->n;
-        e.np = np;
+        e.np = np_alloc;
         e.kp = kp;
         e.n_rt = n_rt;
         e.n_ct = nct;
@@ -1109,7 +1154,7 @@ int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_sta
         STO_CUDA(cudaMemsetAsync(P->ex_bar, 0, sizeof(unsigned long long) * 32 * nct, s));
         const int g = std::min(grid, n_rt * nct);
         void *args[] = {(void *)&e};
-        STO_CUDA(cudaLaunchCooperativeKernel((void *)ens_exact_kernel, dim3(g), dim3(kExThreads), args, smem, s));
+        STO_CUDA(cudaLaunchCooperativeKernel(fn, dim3(g), dim3(ex_threads(BV)), args, smem, s));
     }
     if (!status) return STO_OK;
     StatusDev h{};

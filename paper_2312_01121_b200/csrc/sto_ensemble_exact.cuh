@@ -42,43 +42,45 @@
 
 namespace sto {
 
-constexpr int kExTR = 32;       // oscillators per tile
 constexpr int kExTB = 64;       // members per tile
-constexpr int kExThreads = 256; // 8 warps
-constexpr int kExKC = 32;       // K chunk = one leaf
-constexpr int kExWP = 34;       // W chunk row pitch (doubles)
-constexpr int kExStages = 3;    // cp.async ring depth
-constexpr int kExOut = 8;       // outputs per thread
-constexpr int kExMaxLevels = 8;   // leaf stack depth: ceil(n/32) < 256 leaves (n <= 8160)
-constexpr int kExMaxTiles = 63;   // tiles per CTA and launch
-constexpr int kExPlanes = 12;     // m, s, acc, k3 (x, y, z each)
-constexpr int kExChunkW = kExTR * kExWP;       // doubles
-constexpr int kExChunkX = kExKC * kExTB;       // doubles
+constexpr int kExThreads = 256; // threads per CTA with 2 members per thread (512 with 1)
+constexpr int kExDefaultBV = 2; // members per thread (host default; STO_EX_BV overrides): 2 measured
+                                // 9.9e8 vs 7.9e8 osc-steps/s with 1 (16 warps at 128 registers, spills)
+constexpr int kExKC = 32;       // K chunk (a leaf is two chunks: 64 columns)
+constexpr int kExWP = 34;       // W chunk row pitch (doubles): conflict-free 16-byte row reads
+constexpr int kExStages = 2;    // cp.async ring depth
+constexpr int kExMaxU = 7;      // rows per thread (tile = 8U oscillators)
+constexpr int kExMaxLevels = 8; // leaf stack depth: ceil(n/64) < 256 leaves (n <= 16320)
+constexpr int kExMaxTiles = 63; // tiles per CTA and launch
+constexpr int kExPlanes = 12;   // m, s, acc, k3 (x, y, z each)
+constexpr int kExChunkX = kExKC * kExTB;  // doubles
 
-__host__ __device__ constexpr size_t ex_smem_bytes(int levels) {
-    return sizeof(double) * ((size_t)kExStages * (kExChunkW + kExChunkX) +
-                             (size_t)levels * kExOut * kExThreads + kExTB * 11 + kExTR) +
+__host__ __device__ constexpr int ex_chunk_w(int u) { return 8 * u * kExWP; }
+// the leaf stack holds levels doubles per output: 8U x 64 outputs per tile
+__host__ __device__ constexpr size_t ex_smem_bytes(int u, int levels) {
+    return sizeof(double) * ((size_t)kExStages * (ex_chunk_w(u) + kExChunkX) +
+                             (size_t)levels * 8 * u * kExTB + kExTB * 11 + 8 * u) +
            64;
 }
-
-static_assert(ex_smem_bytes(kExMaxLevels) <= 227 * 1024, "exact ensemble shared memory budget");
+__host__ __device__ constexpr int ex_threads(int bv) { return kExThreads * 2 / bv; }
+constexpr size_t kExSmemBudget = 227 * 1024;
 
 struct ExParams {
-    int n, np, kp;                // oscillators; padded rows (multiple of 32); K padded (multiple of 32)
-    int n_rt, n_ct;               // row tiles, member tiles
+    int n, np, kp;                // oscillators; allocated rows; K padded (multiple of 32)
+    int n_rt, n_ct;               // row tiles, member tiles of this launch
     int batch, bp;                // members of this launch; padded (multiple of 64)
     int member0, batch_total;     // first member of this launch; members of the run
-    int n_in, levels;             // leaf-stack depth (>= ceil(log2(kp / 32)))
+    int n_in, levels;             // leaf-stack depth (bit length of the leaf count)
     const double *w;              // np x kp row-major, -0.0 padded
     const double *w_in;           // n x n_in
-    const double *consts;         // (batch, 11)
-    double *m;                    // (batch, n, 3) in/out
+    const double *consts;         // (batch_total, 11)
+    double *m;                    // (batch_total, n, 3) in/out
     const double *samples;        // member b: samples + b * sample_member_stride
     long long sample_member_stride;
     long long n_samples, sps;
     double dt, h2, dt6;
     long long steps, stride, n_records;
-    double *states;               // (n_records, batch, n, 3) or null
+    double *states;               // (n_records, batch_total, n, 3) or null
     double *x;                    // [2][kp][bp] stage x, +0.0 padded
     double *st;                   // [12][np][bp] RK state planes
     unsigned long long *bar;      // per member tile: [0] counter, [1] stop word (32 words apart)
@@ -94,16 +96,25 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__global__ void __launch_bounds__(kExThreads, 1) ens_exact_kernel(const __grid_constant__ ExParams p) {
+// U: oscillator rows per thread, BV: members per thread; tile = TR = 8U
+// oscillators x 64 members, NT = 512 / BV threads; output o = BV*i + e of lane
+// (lr = lane & 7, lb = lane >> 3) of warp w is oscillator lr + 8i, member
+// 4BV*w + BV*lb + e.
+template <int U, int BV>
+__global__ void __launch_bounds__(ex_threads(BV), 1) ens_exact_kernel(const __grid_constant__ ExParams p) {
+    constexpr int TR = 8 * U;
+    constexpr int NT = ex_threads(BV);
+    constexpr int NO = BV * U;                      // outputs per thread
+    constexpr int CW = ex_chunk_w(U);
     extern __shared__ __align__(16) double smem[];
-    double *ring = smem;                                           // kExStages x (W chunk | X chunk)
-    double *stk = ring + kExStages * (kExChunkW + kExChunkX);      // [levels][kExOut][threads]
-    double *cs = stk + (size_t)p.levels * kExOut * kExThreads;     // [64][11] member consts of the tile
-    double *wins = cs + kExTB * 11;                                // [32] input weights (n_in = 1)
-    volatile int *sh_stop = reinterpret_cast<volatile int *>(wins + kExTR);
+    double *ring = smem;                            // kExStages x (W chunk | X chunk)
+    double *stk = ring + kExStages * (CW + kExChunkX);  // [levels][NO][threads]
+    double *cs = stk + (size_t)p.levels * NO * NT;  // [64][11] member consts of the tile
+    double *wins = cs + kExTB * 11;                 // [TR] input weights (n_in = 1)
+    volatile int *sh_stop = reinterpret_cast<volatile int *>(wins + TR);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wr = warp & 3, wb = warp >> 2, lr = lane & 3, lb = lane >> 2;
+    const int lr = lane & 7, lb = lane >> 3;
     const int n_tiles = p.n_rt * p.n_ct;
     const int n_chunks = p.kp / kExKC;
     const long long n_stages = 4 * p.steps;
@@ -112,18 +123,16 @@ __global__ void __launch_bounds__(kExThreads, 1) ens_exact_kernel(const __grid_c
     int my_tiles = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) ++my_tiles;
     unsigned long long stopped = 0;  // bit i: this CTA's i-th tile has stopped (record-step stop)
-
-    // local row / member of output o = (i, j, e): o = 4i + 2j + e
-    auto row_of = [&](int i) { return 8 * wr + lr + 4 * i; };
-    auto mem_of = [&](int j, int e) { return 32 * wb + 16 * j + 2 * lb + e; };
+    auto row_of = [&](int i) { return lr + 8 * i; };
+    const int mcol = 4 * BV * warp + BV * lb;  // first of this lane's members (tile-local)
 
     // ---- prologue: state planes, x(0), record 0 --------------------------------
     for (int ti = 0; ti < my_tiles; ++ti) {
         const int t = blockIdx.x + ti * gridDim.x;
         const int rt = t % p.n_rt, ct = t / p.n_rt;
-        for (int i = tid; i < kExTR * kExTB; i += kExThreads) {
+        for (int i = tid; i < TR * kExTB; i += NT) {
             const int rl = i / kExTB, bl = i % kExTB;
-            const int k = rt * kExTR + rl, bg = ct * kExTB + bl;
+            const int k = rt * TR + rl, bg = ct * kExTB + bl;
             if (k >= p.n || bg >= p.batch) continue;
             const double *mm = p.m + ((size_t)(p.member0 + bg) * p.n + k) * 3;
             const double mx = mm[0], my = mm[1], mz = mm[2];
@@ -157,7 +166,7 @@ __global__ void __launch_bounds__(kExThreads, 1) ens_exact_kernel(const __grid_c
             if (stopped >> ti & 1ull) continue;
             const int t = blockIdx.x + ti * gridDim.x;
             const int rt = t % p.n_rt, ct = t / p.n_rt;
-            const int row0 = rt * kExTR, col0 = ct * kExTB;
+            const int row0 = rt * TR, col0 = ct * kExTB;
             unsigned long long *bar = p.bar + 32 * ct;
             // ---- wait until every row tile of this member column published x(g)
             if (tid == 0) {
@@ -172,11 +181,11 @@ __global__ void __launch_bounds__(kExThreads, 1) ens_exact_kernel(const __grid_c
                 *sh_stop = (g > 0 && (g & 3) == 0) ? (int)*((volatile unsigned long long *)bar + 1) : 0;
             }
             // member constants and input weights of this tile
-            for (int i = tid; i < kExTB * 11; i += kExThreads) {
+            for (int i = tid; i < kExTB * 11; i += NT) {
                 const int b = p.member0 + min(col0 + i / 11, p.batch - 1);
                 cs[i] = p.consts[(size_t)b * 11 + i % 11];
             }
-            for (int i = tid; i < kExTR; i += kExThreads)
+            for (int i = tid; i < TR; i += NT)
                 wins[i] = (row0 + i < p.n) ? p.w_in[(size_t)(row0 + i) * p.n_in] : 0.0;
             __syncthreads();
             if (*sh_stop) {  // the column stopped after the previous (recording) step
@@ -185,95 +194,101 @@ __global__ void __launch_bounds__(kExThreads, 1) ens_exact_kernel(const __grid_c
                 continue;
             }
 
-            // ---- K loop: leaves of 32 columns through the cp.async ring ---------
+            // ---- K loop: 32-column chunks through the cp.async ring --------------
             const double *xsrc = p.x + (size_t)(g & 1) * xplane;
             auto issue = [&](int ch) {
-                double *slot = ring + (ch % kExStages) * (kExChunkW + kExChunkX);
+                double *slot = ring + (ch % kExStages) * (CW + kExChunkX);
                 const int c0 = ch * kExKC;
-                // W: 32 rows x 32 cols -> pitch 34; 16 x 16-byte pieces per row
-                for (int i = tid; i < kExTR * (kExKC / 2); i += kExThreads) {
+                for (int i = tid; i < TR * (kExKC / 2); i += NT) {
                     const int r = i / (kExKC / 2), q = i % (kExKC / 2);
                     cp_async16(slot + r * kExWP + 2 * q, p.w + (size_t)(row0 + r) * p.kp + c0 + 2 * q);
                 }
-                // X: 32 cols x 64 members; 32 pieces per column row
-                double *xs = slot + kExChunkW;
-                for (int i = tid; i < kExKC * (kExTB / 2); i += kExThreads) {
+                double *xs = slot + CW;
+                for (int i = tid; i < kExKC * (kExTB / 2); i += NT) {
                     const int c = i / (kExTB / 2), q = i % (kExTB / 2);
                     cp_async16(xs + c * kExTB + 2 * q, xsrc + (size_t)(c0 + c) * p.bp + col0 + 2 * q);
                 }
             };
             issue(0);
             cp_async_commit();
-            if (n_chunks > 1) issue(1);
-            cp_async_commit();
+            double pend[NO];  // node of the leaf's first chunk (leaf = two chunks)
             for (int ch = 0; ch < n_chunks; ++ch) {
-                cp_async_wait<1>();
-                __syncthreads();  // chunk ch visible to all; slot (ch + 2) % 3 free (read in ch - 1)
-                if (ch + 2 < n_chunks) issue(ch + 2);
+                cp_async_wait<0>();
+                __syncthreads();  // chunk ch visible to all; the other slot (read in ch - 1) is free
+                if (ch + 1 < n_chunks) issue(ch + 1);
                 cp_async_commit();
-                const double *Ws = ring + (ch % kExStages) * (kExChunkW + kExChunkX);
-                const double *Xs = Ws + kExChunkW;
-                double t1[kExOut], t4[kExOut], tq[kExOut];
+                const double *Ws = ring + (ch % kExStages) * (CW + kExChunkX);
+                const double *Xs = Ws + CW;
+                double t1[NO], t4[NO], tq[NO];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {  // 4-column sub-blocks of the leaf
+                for (int q = 0; q < 8; ++q) {  // 4-column sub-blocks of the chunk
                     const int c0 = 4 * q;
-                    double2 wa[2][2], xa[4][2];
+                    double xa[4][BV];
 #pragma unroll
-                    for (int i = 0; i < 2; ++i) {
-                        wa[i][0] = *reinterpret_cast<const double2 *>(Ws + row_of(i) * kExWP + c0);
-                        wa[i][1] = *reinterpret_cast<const double2 *>(Ws + row_of(i) * kExWP + c0 + 2);
+                    for (int cc = 0; cc < 4; ++cc) {
+                        if constexpr (BV == 2) {
+                            const double2 v = *reinterpret_cast<const double2 *>(Xs + (c0 + cc) * kExTB + mcol);
+                            xa[cc][0] = v.x;
+                            xa[cc][BV - 1] = v.y;
+                        } else {
+                            xa[cc][0] = Xs[(c0 + cc) * kExTB + mcol];
+                        }
                     }
 #pragma unroll
-                    for (int cc = 0; cc < 4; ++cc)
+                    for (int i = 0; i < U; ++i) {
+                        const double2 w01 = *reinterpret_cast<const double2 *>(Ws + row_of(i) * kExWP + c0);
+                        const double2 w23 = *reinterpret_cast<const double2 *>(Ws + row_of(i) * kExWP + c0 + 2);
 #pragma unroll
-                        for (int j = 0; j < 2; ++j)
-                            xa[cc][j] = *reinterpret_cast<const double2 *>(Xs + (c0 + cc) * kExTB + mem_of(j, 0));
-#pragma unroll
-                    for (int i = 0; i < 2; ++i)
-#pragma unroll
-                        for (int j = 0; j < 2; ++j)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const int o = 4 * i + 2 * j + e;
-                                const double x0 = e ? xa[0][j].y : xa[0][j].x, x1 = e ? xa[1][j].y : xa[1][j].x;
-                                const double x2 = e ? xa[2][j].y : xa[2][j].x, x3 = e ? xa[3][j].y : xa[3][j].x;
-                                const double n4 = radd(radd(rmul(wa[i][0].x, x0), rmul(wa[i][0].y, x1)),
-                                                       radd(rmul(wa[i][1].x, x2), rmul(wa[i][1].y, x3)));
-                                // aligned 32-tree over the 8 node4s, unrolled:
-                                // ((n0+n1)+(n2+n3)) + ((n4+n5)+(n6+n7))
-                                switch (q) {
-                                    case 0: tq[o] = n4; break;
-                                    case 1: t1[o] = radd(tq[o], n4); break;
-                                    case 2: tq[o] = n4; break;
-                                    case 3: t1[o] = radd(t1[o], radd(tq[o], n4)); break;
-                                    case 4: tq[o] = n4; break;
-                                    case 5: t4[o] = radd(tq[o], n4); break;
-                                    case 6: tq[o] = n4; break;
-                                    default: t4[o] = radd(t4[o], radd(tq[o], n4)); break;
-                                }
+                        for (int e = 0; e < BV; ++e) {
+                            const int o = BV * i + e;
+                            const double x0 = xa[0][e], x1 = xa[1][e], x2 = xa[2][e], x3 = xa[3][e];
+                            const double n4 = radd(radd(rmul(w01.x, x0), rmul(w01.y, x1)),
+                                                   radd(rmul(w23.x, x2), rmul(w23.y, x3)));
+                            // aligned 32-tree over the 8 node4s, unrolled:
+                            // ((n0+n1)+(n2+n3)) + ((n4+n5)+(n6+n7))
+                            switch (q) {
+                                case 0: tq[o] = n4; break;
+                                case 1: t1[o] = radd(tq[o], n4); break;
+                                case 2: tq[o] = n4; break;
+                                case 3: t1[o] = radd(t1[o], radd(tq[o], n4)); break;
+                                case 4: tq[o] = n4; break;
+                                case 5: t4[o] = radd(tq[o], n4); break;
+                                case 6: tq[o] = n4; break;
+                                default: t4[o] = radd(t4[o], radd(tq[o], n4)); break;
                             }
-                }
-                // leaf -> binary-counter stack (left sibling first), tree_dot_stream order
-#pragma unroll
-                for (int o = 0; o < kExOut; ++o) {
-                    double v = radd(t1[o], t4[o]);
-                    int lvl = 0;
-                    while ((unsigned)ch & (1u << lvl)) {
-                        v = radd(stk[((size_t)lvl * kExOut + o) * kExThreads + tid], v);
-                        ++lvl;
+                        }
                     }
-                    stk[((size_t)lvl * kExOut + o) * kExThreads + tid] = v;
+                }
+                if (!(ch & 1) && ch + 1 < n_chunks) {
+#pragma unroll
+                    for (int o = 0; o < NO; ++o) pend[o] = radd(t1[o], t4[o]);
+                } else {
+                    // leaf (64 columns; a lone last chunk is the whole leaf: its right
+                    // half is -0.0) -> binary-counter stack, tree_dot_stream order
+                    const unsigned lf = (unsigned)ch >> 1;
+#pragma unroll
+                    for (int o = 0; o < NO; ++o) {
+                        const double c32 = radd(t1[o], t4[o]);
+                        double v = (ch & 1) ? radd(pend[o], c32) : c32;
+                        int lvl = 0;
+                        while (lf & (1u << lvl)) {
+                            v = radd(stk[((size_t)lvl * NO + o) * NT + tid], v);
+                            ++lvl;
+                        }
+                        stk[((size_t)lvl * NO + o) * NT + tid] = v;
+                    }
                 }
             }
             // ---- fold the stack's right edge: cp per output -------------------------
-            double cp[kExOut];
+            const unsigned n_leaves = (unsigned)(n_chunks + 1) >> 1;
+            double cp[NO];
 #pragma unroll
-            for (int o = 0; o < kExOut; ++o) {
+            for (int o = 0; o < NO; ++o) {
                 double acc = 0.0;
                 bool have = false;
                 for (int lvl = 0; lvl < p.levels; ++lvl) {
-                    if ((unsigned)n_chunks & (1u << lvl)) {
-                        const double s = stk[((size_t)lvl * kExOut + o) * kExThreads + tid];
+                    if (n_leaves & (1u << lvl)) {
+                        const double s = stk[((size_t)lvl * NO + o) * NT + tid];
                         acc = have ? radd(s, acc) : s;
                         have = true;
                     }
@@ -285,9 +300,9 @@ __global__ void __launch_bounds__(kExThreads, 1) ens_exact_kernel(const __grid_c
             double *xdst = p.x + (size_t)((g + 1) & 1) * xplane;
             const bool last_stage = g + 1 == n_stages;
 #pragma unroll
-            for (int o = 0; o < kExOut; ++o) {
-                const int i = o >> 2, j = (o >> 1) & 1, e = o & 1;
-                const int rl = row_of(i), bl = mem_of(j, e);
+            for (int o = 0; o < NO; ++o) {
+                const int i = o / BV, e = o % BV;
+                const int rl = row_of(i), bl = mcol + e;
                 const int k = row0 + rl, bg = col0 + bl;
                 if (k >= p.n || bg >= p.batch) continue;
                 const double *cb = cs + bl * 11;
@@ -311,19 +326,19 @@ __global__ void __launch_bounds__(kExThreads, 1) ens_exact_kernel(const __grid_c
                 double xpub;
                 if (stage == 0) {
                     st3(6, d);
-                    const V3 s = stage_point(m, d, p.h2);
-                    st3(3, s);
-                    xpub = s.x;
+                    const V3 sv = stage_point(m, d, p.h2);
+                    st3(3, sv);
+                    xpub = sv.x;
                 } else if (stage == 1) {
                     st3(6, acc_k2(ld3(6), d));
-                    const V3 s = stage_point(m, d, h);
-                    st3(3, s);
-                    xpub = s.x;
+                    const V3 sv = stage_point(m, d, h);
+                    st3(3, sv);
+                    xpub = sv.x;
                 } else if (stage == 2) {
                     st3(9, d);
-                    const V3 s = stage_point(m, d, h);
-                    st3(3, s);
-                    xpub = s.x;
+                    const V3 sv = stage_point(m, d, h);
+                    st3(3, sv);
+                    xpub = sv.x;
                 } else {
                     const V3 mn = rk4_final(m, ld3(6), ld3(9), d, p.dt6);
                     st3(0, mn);

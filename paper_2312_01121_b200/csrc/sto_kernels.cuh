@@ -136,9 +136,12 @@ __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInf
                                            int lcta, unsigned long long local_target,
                                            unsigned long long epoch, bool record_stage,
                                            const StatusDev *status, volatile int *sflag) {
+    // One system-scope fence per role (each costs a round to the peers): the CTA's
+    // release of its peer stores, the leader's release of its flags (then plain
+    // relaxed stores), and ONE acquire after thread 0 has seen every flag.
     __syncthreads();
     if (threadIdx.x == 0) {
-        asm volatile("fence.sc.sys;" ::: "memory");  // our peer stores are system-visible
+        asm volatile("fence.acq_rel.sys;" ::: "memory");  // our peer stores are system-visible
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(sh.bar) : "memory");
         unsigned long long v;
         do {
@@ -150,44 +153,48 @@ __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInf
             // recording step is already in the (local) status
             const bool diverged = record_stage && *((volatile const int32_t *)&status->flag) != 0;
             const unsigned long long f = epoch | (diverged ? (1ull << 63) : 0ull);
+            asm volatile("fence.acq_rel.sys;" ::: "memory");  // release pattern: fence + relaxed stores
             for (int q = 0; q < mp.world; ++q)
-                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(mp.flags_of[q] + (size_t)rank * kFlagSlot),
+                asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(mp.flags_of[q] + (size_t)rank * kFlagSlot),
                              "l"(f)
                              : "memory");
         }
-    }
-    if (threadIdx.x < mp.world) {
-        unsigned long long f, t0 = 0;
+        unsigned long long t0 = 0;
         bool stop = false;
-        for (unsigned it = 0;; ++it) {
-            asm volatile("ld.relaxed.sys.global.u64 %0, [%1];"
-                         : "=l"(f)
-                         : "l"(sh.flags + (size_t)threadIdx.x * kFlagSlot)
-                         : "memory");
-            const unsigned long long fe = f & ~(1ull << 63);
-            if (fe >= epoch) {
-                // A peer may already be ONE epoch ahead (it passed this exchange
-                // and raised the next flag before we polled).  Its stop bit then
-                // belongs to that next exchange: honour it only on the epoch it
-                // was raised for, so that every rank stops after the same
-                // exchange (else this rank would stop one exchange early and the
-                // peer would wait for our next flag forever).
-                stop = (f >> 63) && fe == epoch;
-                break;
+        unsigned pending = (mp.world >= 32 ? 0xffffffffu : (1u << mp.world) - 1u);
+        for (unsigned it = 0; pending; ++it) {
+            for (int q = 0; q < mp.world; ++q) {
+                if (!(pending >> q & 1u)) continue;
+                unsigned long long f;
+                asm volatile("ld.relaxed.sys.global.u64 %0, [%1];"
+                             : "=l"(f)
+                             : "l"(sh.flags + (size_t)q * kFlagSlot)
+                             : "memory");
+                const unsigned long long fe = f & ~(1ull << 63);
+                if (fe >= epoch) {
+                    // A peer may already be ONE epoch ahead (it passed this exchange
+                    // and raised the next flag before we polled).  Its stop bit then
+                    // belongs to that next exchange: honour it only on the epoch it
+                    // was raised for, so that every rank stops after the same
+                    // exchange (else this rank would stop one exchange early and the
+                    // peer would wait for our next flag forever).
+                    stop |= (f >> 63) && fe == epoch;
+                    pending &= ~(1u << q);
+                }
             }
             // watchdog: a peer that never arrives (its process died or never
             // launched) must not hang this GPU -- report it and stop
-            if ((it & 1023u) == 1023u) {
+            if (pending && (it & 1023u) == 1023u) {
                 const unsigned long long t = globaltimer_ns();
                 if (t0 == 0) t0 = t;
                 else if (t - t0 > mp.timeout_ns) {
-                    report_peer_timeout(const_cast<StatusDev *>(status), threadIdx.x);
+                    report_peer_timeout(const_cast<StatusDev *>(status), __ffs(pending) - 1);
                     stop = true;
                     break;
                 }
             }
         }
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        asm volatile("fence.acq_rel.sys;" ::: "memory");  // acquire: every peer's x is visible
         if (stop) *sflag = 1;
     }
     __syncthreads();
@@ -327,12 +334,30 @@ __global__ void __launch_bounds__(NT, 1) grid_rk4_kernel(const __grid_constant__
                     // the receive buffer is in LOGICAL order (each rank pushes its
                     // contiguous row slice as 16-byte vectors); the physical window
                     // [x_base, x_base + x_len) holds exactly the logical columns of the
-                    // same range (segments are contiguous), permuted -- scatter them,
-                    // +0.0 for the padding columns k >= n
+                    // same range (segments are contiguous), permuted.  Walk it in
+                    // PHYSICAL order, one 16-byte slot per thread (conflict-free shared
+                    // stores): slot m of a segment of C columns per lane holds the
+                    // logical pair base + (m & 31) * C + 2 (m >> 5), +1; +0.0 for k >= n
                     const double *src = xrecv + (size_t)((p.mp.epoch_base + e) & 1) * cs.ldw;
-                    for (int i = threadIdx.x; i < x_len; i += blockDim.x) {
-                        const int k = x_base + i;
-                        xs[col_perm(cs, k) - x_base] = (k < cs.n) ? __ldcg(src + k) : 0.0;
+                    const int full_end = cs.nfull * kSegFull;
+                    for (int i = threadIdx.x; i < x_len / 2; i += blockDim.x) {
+                        const int pos = x_base + 2 * i;
+                        int base, c;
+                        if (pos < full_end) {
+                            base = pos & ~(kSegFull - 1);
+                            c = 16;
+                        } else {
+                            int t = cs.ntail - 1;
+                            while (t > 0 && pos < cs.tail_base[t]) --t;
+                            base = cs.tail_base[t];
+                            c = cs.tail_c[t];
+                        }
+                        const int mi = (pos - base) >> 1;
+                        const int k = base + (mi & 31) * c + 2 * (mi >> 5);
+                        double2 v;
+                        if (k + 1 < cs.n) v = __ldcg(reinterpret_cast<const double2 *>(src + k));
+                        else v = make_double2(k < cs.n ? __ldcg(src + k) : 0.0, 0.0);
+                        reinterpret_cast<double2 *>(xs)[i] = v;
                     }
                 } else {
                     const double *src = xrecv + (size_t)(e & 1) * cs.ldw + x_base;

@@ -90,6 +90,18 @@ def test_multichannel_and_per_member_drives(sto, oracle_mod):
     _check(sto, oracle_mod, top, _sweep(sto, batch), cfg, range(batch), series=series)
 
 
+@pytest.mark.parametrize("u", [1, 2, 3, 4, 5, 6, 7])
+def test_every_tile_height(sto, oracle_mod, monkeypatch, u):
+    """Tiles of 8U oscillators x 64 members (the host picks U per size; every
+    U forced here) at a ragged n with several row tiles."""
+    monkeypatch.setenv("STO_EX_U", str(u))
+    n, batch = 203, 70
+    top = _rand_top(sto, n, seed=u)
+    series = sto.InputSeries(np.random.default_rng(u).uniform(-1, 1, (30, 1)), 2)
+    cfg = sto.RunConfig(n=n, steps=60, dt=1e-11, record_stride=20, input_series=series)
+    _check(sto, oracle_mod, top, _sweep(sto, batch), cfg, (0, 37, 64, 69))
+
+
 def test_several_launches(sto, oracle_mod, monkeypatch):
     monkeypatch.setenv("STO_EX_CT_PER_LAUNCH", "1")
     n, batch = 64, 150
