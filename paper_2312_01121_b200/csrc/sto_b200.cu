@@ -1044,7 +1044,9 @@ const void *ex_kernel_bv(int u) {
         default: return (const void *)ens_exact_kernel<7, BV>;
     }
 }
-const void *ex_kernel_of(int u, int bv) { return bv == 2 ? ex_kernel_bv<2>(u) : ex_kernel_bv<1>(u); }
+const void *ex_kernel_of(int u, int bv) {
+    return bv == 4 ? ex_kernel_bv<4>(u) : (bv == 2 ? ex_kernel_bv<2>(u) : ex_kernel_bv<1>(u));
+}
 }  // namespace
 
 extern "C" {
@@ -1067,12 +1069,16 @@ int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_sta
     // Tile = 8U oscillators x 64 members, one CTA per SM, several tiles per CTA:
     // minimise the per-CTA work U * ceil(tiles / grid) (ties -> larger U), among
     // the U whose leaf stack fits shared memory.
+    // members per thread: BV = 2 (tiles of 64 members) unless STO_EX_BV says otherwise
+    int BV = kExDefaultBV;
+    if (const char *ev = getenv("STO_EX_BV")) BV = atoi(ev) == 1 ? 1 : (atoi(ev) == 4 ? 4 : 2);
+    const int TB = ex_tile_members(BV);
     const int nu = (P->n + 7) / 8;
-    const int total_ct = (int)((r->batch + kExTB - 1) / kExTB);
+    const int total_ct = (int)((r->batch + TB - 1) / TB);
     int U = 0;
     long long best = 0;
     for (int u = 1; u <= kExMaxU; ++u) {
-        if (ex_smem_bytes(u, levels) > kExSmemBudget) continue;
+        if (ex_smem_bytes(u, BV, levels) > kExSmemBudget) continue;
         const long long tiles = (long long)((nu + u - 1) / u) * total_ct;
         const long long cost = (long long)u * ((tiles + P->sm_count - 1) / P->sm_count);
         if (!U || cost <= best) {
@@ -1083,7 +1089,7 @@ int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_sta
     if (!U) return fail(STO_E_PARAM, "exact ensemble: no tile fits shared memory");
     if (const char *ev = getenv("STO_EX_U")) {  // test knob: force a tile height
         const int u = atoi(ev);
-        if (u >= 1 && u <= kExMaxU && ex_smem_bytes(u, levels) <= kExSmemBudget) U = u;
+        if (u >= 1 && u <= kExMaxU && ex_smem_bytes(u, BV, levels) <= kExSmemBudget) U = u;
     }
     const int TR = 8 * U;
     const int n_rt = (P->n + TR - 1) / TR;
@@ -1094,7 +1100,7 @@ int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_sta
     if (const char *ev = getenv("STO_EX_CT_PER_LAUNCH"))  // test knob: force several launches
         ct_per_launch = std::max(1, std::min(ct_per_launch, atoi(ev)));
     if (ct_per_launch > 4096) return fail(STO_E_PARAM, "too many member tiles");
-    const size_t bp = (size_t)ct_per_launch * kExTB;
+    const size_t bp = (size_t)ct_per_launch * TB;
     if (!P->ex_w) {
         STO_CUDA(cudaMalloc(&P->ex_w, sizeof(double) * (size_t)np_alloc * kp));
         STO_CUDA(cudaMalloc(&P->ex_bar, sizeof(unsigned long long) * 32 * 4096));
@@ -1109,10 +1115,7 @@ int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_sta
         STO_CUDA(cudaMalloc(&P->ex_st, sizeof(double) * kExPlanes * np_alloc * bp));
         P->ex_bp = bp;
     }
-    const size_t smem = ex_smem_bytes(U, levels);
-    // members per thread: 1 (16 warps, more latency hiding) or 2 (8 warps)
-    int BV = kExDefaultBV;
-    if (const char *ev = getenv("STO_EX_BV")) BV = atoi(ev) == 2 ? 2 : 1;
+    const size_t smem = ex_smem_bytes(U, BV, levels);
     const void *fn = ex_kernel_of(U, BV);
     STO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     reset_status_kernel<<<1, 256, 0, s>>>(P->status, P->bar, P->flags);
@@ -1125,8 +1128,8 @@ int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_sta
         e.kp = kp;
         e.n_rt = n_rt;
         e.n_ct = nct;
-        e.member0 = c0 * kExTB;
-        e.batch = (int)std::min<int64_t>((int64_t)nct * kExTB, r->batch - e.member0);
+        e.member0 = c0 * TB;
+        e.batch = (int)std::min<int64_t>((int64_t)nct * TB, r->batch - e.member0);
         e.batch_total = (int)r->batch;
         e.bp = (int)bp;
         e.n_in = P->n_in;
@@ -1154,7 +1157,7 @@ int sto_integrate_ensemble_exact(sto_plan *P, const sto_ensemble_run *r, sto_sta
         STO_CUDA(cudaMemsetAsync(P->ex_bar, 0, sizeof(unsigned long long) * 32 * nct, s));
         const int g = std::min(grid, n_rt * nct);
         void *args[] = {(void *)&e};
-        STO_CUDA(cudaLaunchCooperativeKernel(fn, dim3(g), dim3(ex_threads(BV)), args, smem, s));
+        STO_CUDA(cudaLaunchCooperativeKernel(fn, dim3(g), dim3(kExThreads), args, smem, s));
     }
     if (!status) return STO_OK;
     StatusDev h{};

@@ -42,10 +42,8 @@
 
 namespace sto {
 
-constexpr int kExTB = 64;       // members per tile
-constexpr int kExThreads = 256; // threads per CTA with 2 members per thread (512 with 1)
-constexpr int kExDefaultBV = 2; // members per thread (host default; STO_EX_BV overrides): 2 measured
-                                // 9.9e8 vs 7.9e8 osc-steps/s with 1 (16 warps at 128 registers, spills)
+constexpr int kExThreads = 256; // threads per CTA (8 warps)
+constexpr int kExDefaultBV = 2; // members per thread (host default; STO_EX_BV overrides)
 constexpr int kExKC = 32;       // K chunk (a leaf is two chunks: 64 columns)
 constexpr int kExWP = 34;       // W chunk row pitch (doubles): conflict-free 16-byte row reads
 constexpr int kExStages = 2;    // cp.async ring depth
@@ -53,16 +51,16 @@ constexpr int kExMaxU = 7;      // rows per thread (tile = 8U oscillators)
 constexpr int kExMaxLevels = 8; // leaf stack depth: ceil(n/64) < 256 leaves (n <= 16320)
 constexpr int kExMaxTiles = 63; // tiles per CTA and launch
 constexpr int kExPlanes = 12;   // m, s, acc, k3 (x, y, z each)
-constexpr int kExChunkX = kExKC * kExTB;  // doubles
 
 __host__ __device__ constexpr int ex_chunk_w(int u) { return 8 * u * kExWP; }
-// the leaf stack holds levels doubles per output: 8U x 64 outputs per tile
-__host__ __device__ constexpr size_t ex_smem_bytes(int u, int levels) {
-    return sizeof(double) * ((size_t)kExStages * (ex_chunk_w(u) + kExChunkX) +
-                             (size_t)levels * 8 * u * kExTB + kExTB * 11 + 8 * u) +
+__host__ __device__ constexpr int ex_tile_members(int bv) { return 32 * bv; }
+// ring (W and x chunks) + leaf stack (levels doubles per output: 8U x 32BV
+// outputs per tile) + member constants + input weights
+__host__ __device__ constexpr size_t ex_smem_bytes(int u, int bv, int levels) {
+    return sizeof(double) * ((size_t)kExStages * (ex_chunk_w(u) + kExKC * ex_tile_members(bv)) +
+                             (size_t)levels * 8 * u * ex_tile_members(bv) + ex_tile_members(bv) * 11 + 8 * u) +
            64;
 }
-__host__ __device__ constexpr int ex_threads(int bv) { return kExThreads * 2 / bv; }
 constexpr size_t kExSmemBudget = 227 * 1024;
 
 struct ExParams {
@@ -97,20 +95,22 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // U: oscillator rows per thread, BV: members per thread; tile = TR = 8U
-// oscillators x 64 members, NT = 512 / BV threads; output o = BV*i + e of lane
+// oscillators x TB = 32BV members, 8 warps; output o = BV*i + e of lane
 // (lr = lane & 7, lb = lane >> 3) of warp w is oscillator lr + 8i, member
 // 4BV*w + BV*lb + e.
 template <int U, int BV>
-__global__ void __launch_bounds__(ex_threads(BV), 1) ens_exact_kernel(const __grid_constant__ ExParams p) {
+__global__ void __launch_bounds__(kExThreads, 1) ens_exact_kernel(const __grid_constant__ ExParams p) {
     constexpr int TR = 8 * U;
-    constexpr int NT = ex_threads(BV);
+    constexpr int TB = ex_tile_members(BV);
+    constexpr int kExChunkX = kExKC * TB;
+    constexpr int NT = kExThreads;
     constexpr int NO = BV * U;                      // outputs per thread
     constexpr int CW = ex_chunk_w(U);
     extern __shared__ __align__(16) double smem[];
     double *ring = smem;                            // kExStages x (W chunk | X chunk)
     double *stk = ring + kExStages * (CW + kExChunkX);  // [levels][NO][threads]
     double *cs = stk + (size_t)p.levels * NO * NT;  // [64][11] member consts of the tile
-    double *wins = cs + kExTB * 11;                 // [TR] input weights (n_in = 1)
+    double *wins = cs + TB * 11;                 // [TR] input weights (n_in = 1)
     volatile int *sh_stop = reinterpret_cast<volatile int *>(wins + TR);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -130,9 +130,9 @@ __global__ void __launch_bounds__(ex_threads(BV), 1) ens_exact_kernel(const __gr
     for (int ti = 0; ti < my_tiles; ++ti) {
         const int t = blockIdx.x + ti * gridDim.x;
         const int rt = t % p.n_rt, ct = t / p.n_rt;
-        for (int i = tid; i < TR * kExTB; i += NT) {
-            const int rl = i / kExTB, bl = i % kExTB;
-            const int k = rt * TR + rl, bg = ct * kExTB + bl;
+        for (int i = tid; i < TR * TB; i += NT) {
+            const int rl = i / TB, bl = i % TB;
+            const int k = rt * TR + rl, bg = ct * TB + bl;
             if (k >= p.n || bg >= p.batch) continue;
             const double *mm = p.m + ((size_t)(p.member0 + bg) * p.n + k) * 3;
             const double mx = mm[0], my = mm[1], mz = mm[2];
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(ex_threads(BV), 1) ens_exact_kernel(const __gr
             if (stopped >> ti & 1ull) continue;
             const int t = blockIdx.x + ti * gridDim.x;
             const int rt = t % p.n_rt, ct = t / p.n_rt;
-            const int row0 = rt * TR, col0 = ct * kExTB;
+            const int row0 = rt * TR, col0 = ct * TB;
             unsigned long long *bar = p.bar + 32 * ct;
             // ---- wait until every row tile of this member column published x(g)
             if (tid == 0) {
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(ex_threads(BV), 1) ens_exact_kernel(const __gr
                 *sh_stop = (g > 0 && (g & 3) == 0) ? (int)*((volatile unsigned long long *)bar + 1) : 0;
             }
             // member constants and input weights of this tile
-            for (int i = tid; i < kExTB * 11; i += NT) {
+            for (int i = tid; i < TB * 11; i += NT) {
                 const int b = p.member0 + min(col0 + i / 11, p.batch - 1);
                 cs[i] = p.consts[(size_t)b * 11 + i % 11];
             }
@@ -204,9 +204,9 @@ __global__ void __launch_bounds__(ex_threads(BV), 1) ens_exact_kernel(const __gr
                     cp_async16(slot + r * kExWP + 2 * q, p.w + (size_t)(row0 + r) * p.kp + c0 + 2 * q);
                 }
                 double *xs = slot + CW;
-                for (int i = tid; i < kExKC * (kExTB / 2); i += NT) {
-                    const int c = i / (kExTB / 2), q = i % (kExTB / 2);
-                    cp_async16(xs + c * kExTB + 2 * q, xsrc + (size_t)(c0 + c) * p.bp + col0 + 2 * q);
+                for (int i = tid; i < kExKC * (TB / 2); i += NT) {
+                    const int c = i / (TB / 2), q = i % (TB / 2);
+                    cp_async16(xs + c * TB + 2 * q, xsrc + (size_t)(c0 + c) * p.bp + col0 + 2 * q);
                 }
             };
             issue(0);
@@ -226,12 +226,15 @@ __global__ void __launch_bounds__(ex_threads(BV), 1) ens_exact_kernel(const __gr
                     double xa[4][BV];
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) {
-                        if constexpr (BV == 2) {
-                            const double2 v = *reinterpret_cast<const double2 *>(Xs + (c0 + cc) * kExTB + mcol);
-                            xa[cc][0] = v.x;
-                            xa[cc][BV - 1] = v.y;
+                        if constexpr (BV == 1) {
+                            xa[cc][0] = Xs[(c0 + cc) * TB + mcol];
                         } else {
-                            xa[cc][0] = Xs[(c0 + cc) * kExTB + mcol];
+#pragma unroll
+                            for (int h = 0; h < BV / 2; ++h) {
+                                const double2 v = *reinterpret_cast<const double2 *>(Xs + (c0 + cc) * TB + mcol + 2 * h);
+                                xa[cc][2 * h] = v.x;
+                                xa[cc][2 * h + 1] = v.y;
+                            }
                         }
                     }
 #pragma unroll

@@ -340,24 +340,37 @@ __global__ void __launch_bounds__(NT, 1) grid_rk4_kernel(const __grid_constant__
                     // logical pair base + (m & 31) * C + 2 (m >> 5), +1; +0.0 for k >= n
                     const double *src = xrecv + (size_t)((p.mp.epoch_base + e) & 1) * cs.ldw;
                     const int full_end = cs.nfull * kSegFull;
-                    for (int i = threadIdx.x; i < x_len / 2; i += blockDim.x) {
-                        const int pos = x_base + 2 * i;
-                        int base, c;
-                        if (pos < full_end) {
-                            base = pos & ~(kSegFull - 1);
-                            c = 16;
-                        } else {
+                    auto logical_of = [&](int pos) {  // first logical column of physical pair slot pos
+                        int base = pos & ~(kSegFull - 1), c = 16;
+                        if (pos >= full_end) {
                             int t = cs.ntail - 1;
                             while (t > 0 && pos < cs.tail_base[t]) --t;
                             base = cs.tail_base[t];
                             c = cs.tail_c[t];
                         }
                         const int mi = (pos - base) >> 1;
-                        const int k = base + (mi & 31) * c + 2 * (mi >> 5);
-                        double2 v;
-                        if (k + 1 < cs.n) v = __ldcg(reinterpret_cast<const double2 *>(src + k));
-                        else v = make_double2(k < cs.n ? __ldcg(src + k) : 0.0, 0.0);
-                        reinterpret_cast<double2 *>(xs)[i] = v;
+                        return base + (mi & 31) * c + 2 * (mi >> 5);
+                    };
+                    // four independent L2 loads in flight per thread before the stores
+                    constexpr int kU = 4;
+                    const int npairs = x_len / 2;
+                    for (int i0 = threadIdx.x; i0 < npairs; i0 += kU * blockDim.x) {
+                        double2 v[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            const int i = i0 + u * blockDim.x;
+                            v[u] = make_double2(0.0, 0.0);
+                            if (i < npairs) {
+                                const int k = logical_of(x_base + 2 * i);
+                                if (k + 1 < cs.n) v[u] = __ldcg(reinterpret_cast<const double2 *>(src + k));
+                                else if (k < cs.n) v[u].x = __ldcg(src + k);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            const int i = i0 + u * blockDim.x;
+                            if (i < npairs) reinterpret_cast<double2 *>(xs)[i] = v[u];
+                        }
                     }
                 } else {
                     const double *src = xrecv + (size_t)(e & 1) * cs.ldw + x_base;
