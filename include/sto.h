@@ -220,6 +220,14 @@ STO_API int sto_gemv(int device, const double *w, int64_t rows, int64_t cols, in
 /* a[i] /= divisor (IEEE), device, asynchronous: `entries /= rho`. */
 STO_API int sto_scale_div(int device, double *a, int64_t count, double divisor, void *stream);
 
+/* out[b] = max over records r and oscillators k of | |states[r][b][k]| - 1 |
+ * for recorded states (outer, members, n, 3): Trajectory.max_norm_drift
+ * (integrator.py:184-185, np.linalg.norm order, bit-identical) computed on the
+ * device, so a densely recorded run does not pay a host pass over its states.
+ * Device pointers (out: `members` doubles), asynchronous. */
+STO_API int sto_norm_drift(int device, const double *states, int64_t outer, int64_t members, int64_t n,
+                           double *out, void *stream);
+
 /* Self-test of the kernels' speculative division (sto_device.cuh rdiv_spec, used
  * for h_s = pref / (1 + lambda m.p), model.py:250 / cpu_jit.py:68): for each i,
  * q[i] = rdiv_spec(a[i], b[i]) and ok[i] = its proof of correct rounding, and

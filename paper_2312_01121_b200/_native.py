@@ -107,6 +107,8 @@ SIGNATURES = {
                                 ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "sto_scale_div": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.c_double, ctypes.c_void_p]),
+    "sto_norm_drift": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "sto_selftest_div": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_void_p]),
@@ -215,6 +217,19 @@ def scale_div(a, divisor: float) -> None:
     """a /= divisor in place (IEEE division) on the device."""
     dev = a.device.index
     check(lib().sto_scale_div(dev, a.data_ptr(), a.numel(), float(divisor), _stream_ptr(dev)))
+
+
+def norm_drift(states, members: int = 1):
+    """max | |m| - 1 | per member of device states (outer, members, n, 3) -> CUDA
+    tensor (members,); Trajectory.max_norm_drift on the device."""
+    import torch
+
+    dev = states.device.index
+    out = torch.empty((members,), dtype=torch.float64, device=states.device)
+    outer = states.numel() // (3 * members * states.shape[-2]) if states.numel() else 0
+    check(lib().sto_norm_drift(dev, states.data_ptr(), outer, members, states.shape[-2],
+                               out.data_ptr(), _stream_ptr(dev)))
+    return out
 
 
 def selftest_div(a, b):

@@ -1449,6 +1449,21 @@ int sto_scale_div(int device, double *a, int64_t count, double divisor, void *st
     return STO_OK;
 }
 
+int sto_norm_drift(int device, const double *states, int64_t outer, int64_t members, int64_t n,
+                   double *out, void *stream) {
+    if (!states || !out || outer < 0 || members < 1 || n < 1 || members >= (1 << 30))
+        return fail(STO_E_PARAM, "sto_norm_drift: bad arguments");
+    STO_CUDA(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)stream;
+    STO_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * members, s));
+    const long long total = outer * members * n;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>(1184, (total + 255) / 256));
+    norm_drift_kernel<<<blocks, 256, 0, s>>>(states, outer, (int)members, n,
+                                             reinterpret_cast<unsigned long long *>(out));
+    STO_CUDA(cudaGetLastError());
+    return STO_OK;
+}
+
 int sto_selftest_div(int device, const double *a, const double *b, int64_t count, double *q,
                      int32_t *ok, double *ref, void *stream) {
     if (!a || !b || !q || !ok || !ref || count < 0) return fail(STO_E_PARAM, "sto_selftest_div: bad arguments");

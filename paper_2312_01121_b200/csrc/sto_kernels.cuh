@@ -693,4 +693,36 @@ __global__ void selftest_div_kernel(const double *__restrict__ a, const double *
     }
 }
 
+// sto_norm_drift: out[b] = max over r < outer, k < n of | |m| - 1 | for the
+// recorded states (outer, members, n, 3) -- the reference's
+// np.abs(np.linalg.norm(states, axis=-1) - 1.0).max() (integrator.py:184-185),
+// evaluated where the states already are.  np.linalg.norm of a 3-vector is
+// sqrt((x*x + y*y) + z*z) with every operation rounded (numpy's reduction over a
+// contiguous axis shorter than its pairwise block; tests/test_host.py pins it),
+// so the value is bit-identical.  max() is order-free; values are >= 0 or NaN,
+// so their bit patterns order like the values (a NaN wins, as in numpy).
+// out must be zeroed by the caller.
+__global__ void norm_drift_kernel(const double *__restrict__ states, long long outer, int members, long long n,
+                                  unsigned long long *__restrict__ out) {
+    const long long per = (long long)members * n;
+    const long long total = outer * per;
+    unsigned long long best = 0ull;
+    int cur = -1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)((i % per) / n);
+        if (b != cur) {
+            if (cur >= 0 && best) atomicMax(out + cur, best);
+            cur = b;
+            best = 0ull;
+        }
+        const double *v = states + 3 * i;
+        const double s = radd(radd(rmul(v[0], v[0]), rmul(v[1], v[1])), rmul(v[2], v[2]));
+        const double d = fabs(rsub(__dsqrt_rn(s), 1.0));
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(d) & ~(1ull << 63);
+        if (bits > best) best = bits;
+    }
+    if (cur >= 0 && best) atomicMax(out + cur, best);
+}
+
 }  // namespace sto

@@ -414,3 +414,15 @@ def test_resume_divergence_reports_global_step(params):
     with pytest.raises(sto.IntegrationDivergedError) as info:
         sto.resume(first, top, params, 20, backend=_Stub(poison), input_series=series)
     assert (info.value.oscillator, info.value.step) == (2, 30)
+
+
+def test_numpy_norm_order_pinned():
+    """Trajectory.max_norm_drift is np.linalg.norm(states, axis=-1) (ref
+    integrator.py:184-185); the device version (sto_norm_drift) evaluates
+    sqrt((x*x + y*y) + z*z) with every operation rounded -- numpy's order for a
+    contiguous 3-element reduction.  Pin it here so a numpy change shows up."""
+    g = np.random.default_rng(0)
+    v = g.uniform(-1, 1, (200_000, 3)) * np.exp2(g.integers(-30, 30, (200_000, 1)))
+    want = np.linalg.norm(v, axis=-1)
+    got = np.sqrt((v[:, 0] * v[:, 0] + v[:, 1] * v[:, 1]) + v[:, 2] * v[:, 2])
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
