@@ -61,6 +61,11 @@ enum KernelMode : int { kIntegrate = 0, kDerivative = 1, kMatvec = 2 };
 // while a peer may be writing them.
 // ----------------------------------------------------------------------------
 constexpr int kMaxRanks = 8;
+// scope of the exchange's fences: "sys" (peers are other GPUs); an A/B build may
+// set "gpu" to measure the logical-rank protocol without system-scope fences
+#ifndef STO_MULTI_SCOPE
+#define STO_MULTI_SCOPE "sys"
+#endif
 constexpr int kFlagSlot = 32;  // u64 words between flag slots (256 B)
 
 struct ShardInfo {
@@ -141,7 +146,7 @@ __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInf
     // relaxed stores), and ONE acquire after thread 0 has seen every flag.
     __syncthreads();
     if (threadIdx.x == 0) {
-        asm volatile("fence.acq_rel.sys;" ::: "memory");  // our peer stores are system-visible
+        asm volatile("fence.acq_rel." STO_MULTI_SCOPE ";" ::: "memory");  // our peer stores are system-visible
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(sh.bar) : "memory");
         unsigned long long v;
         do {
@@ -153,7 +158,7 @@ __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInf
             // recording step is already in the (local) status
             const bool diverged = record_stage && *((volatile const int32_t *)&status->flag) != 0;
             const unsigned long long f = epoch | (diverged ? (1ull << 63) : 0ull);
-            asm volatile("fence.acq_rel.sys;" ::: "memory");  // release pattern: fence + relaxed stores
+            asm volatile("fence.acq_rel." STO_MULTI_SCOPE ";" ::: "memory");  // release pattern: fence + relaxed stores
             for (int q = 0; q < mp.world; ++q)
                 asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(mp.flags_of[q] + (size_t)rank * kFlagSlot),
                              "l"(f)
@@ -194,7 +199,7 @@ __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInf
                 }
             }
         }
-        asm volatile("fence.acq_rel.sys;" ::: "memory");  // acquire: every peer's x is visible
+        asm volatile("fence.acq_rel." STO_MULTI_SCOPE ";" ::: "memory");  // acquire: every peer's x is visible
         if (stop) *sflag = 1;
     }
     __syncthreads();

@@ -20,6 +20,12 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs an sm_100 GPU and libsto_b200.so")
 
 
+def fuzz_examples(default: int) -> int:
+    """Hypothesis examples per fuzz test: STO_FUZZ_SCALE multiplies the default
+    (the long fuzz campaign of profiles/r02*_fuzz.log runs with a large scale)."""
+    return max(1, int(default * float(os.environ.get("STO_FUZZ_SCALE", "1"))))
+
+
 def load_golden(name: str) -> dict:
     with np.load(GOLDEN / name, allow_pickle=False) as z:
         return {k: z[k] for k in z.files}

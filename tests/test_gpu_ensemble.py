@@ -12,6 +12,8 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
+from conftest import fuzz_examples
+
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-10
@@ -260,7 +262,7 @@ from hypothesis import HealthCheck, given, settings  # noqa: E402
 from hypothesis import strategies as st  # noqa: E402
 
 
-@settings(max_examples=30, deadline=None, suppress_health_check=[HealthCheck.too_slow,
+@settings(max_examples=fuzz_examples(30), deadline=None, suppress_health_check=[HealthCheck.too_slow,
                                                                  HealthCheck.function_scoped_fixture])
 @given(n=st.integers(1, 260), batch=st.integers(1, 150), steps=st.integers(1, 80),
        u=st.one_of(st.none(), st.integers(1, 7)), seed=st.integers(0, 2**31 - 1))

@@ -12,7 +12,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import assert_bit_equal
+from conftest import assert_bit_equal, fuzz_examples
 
 pytestmark = pytest.mark.gpu
 
@@ -134,7 +134,7 @@ def test_exact_divergence_reports_first_member_and_stops(sto):
     assert time.perf_counter() - t0 < 2.0
 
 
-@settings(max_examples=25, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=fuzz_examples(25), deadline=None, suppress_health_check=list(HealthCheck))
 @given(n=st.integers(1, 300), batch=st.integers(1, 140), steps=st.integers(1, 60),
        stride=st.integers(1, 25), sps=st.integers(1, 7), seed=st.integers(0, 2**31 - 1))
 def test_random_exact_ensembles(sto, oracle_mod, n, batch, steps, stride, sps, seed):

@@ -17,7 +17,7 @@ import pytest
 from hypothesis import HealthCheck, given, settings
 from hypothesis import strategies as st
 
-from conftest import assert_bit_equal
+from conftest import assert_bit_equal, fuzz_examples
 
 pytestmark = pytest.mark.gpu
 
@@ -55,7 +55,7 @@ def _families(n):
     return fams
 
 
-@settings(max_examples=150, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@settings(max_examples=fuzz_examples(150), deadline=None, suppress_health_check=[HealthCheck.too_slow])
 @given(runs())
 def test_random_runs_bit_exact_every_family(oracle_mod, run):
     import paper_2312_01121_b200 as sto
@@ -88,7 +88,7 @@ def test_random_runs_bit_exact_every_family(oracle_mod, run):
         backend.close()
 
 
-@settings(max_examples=40, deadline=None)
+@settings(max_examples=fuzz_examples(40), deadline=None)
 @given(seed=st.integers(min_value=0, max_value=2**31 - 1))
 def test_device_derivative_is_tangent(seed):
     import paper_2312_01121_b200 as sto

@@ -124,6 +124,22 @@ def test_large_n_streaming_against_oracle(sto, oracle_mod):
     assert_bit_equal(states, want, "n=1e4")
 
 
+def test_benched_config4_full_horizon_bit_exact(sto, oracle_mod):
+    """configs[4] as benched (bench.py n1e4): N = 1e4, seed-0 reservoir (device
+    build, as bench.py uses for large N), 1e3 RK4 steps -- the whole benched
+    horizon, every 100th state bit-identical to the oracle (W streamed from
+    HBM with the L2-resident slice).  ~1 min of 16-thread oracle time."""
+    n, steps, stride = 10_000, 1000, 100
+    top = sto.build_topology_device(n, seed=0)
+    params = sto.PhysicalParams()
+    cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=stride)
+    tr = sto.integrate(top, params, cfg)
+    want, _ = oracle_mod.integrate(top.coupling.entries, top.input_weights.entries,
+                                   sto.kernel_scalars(params), sto.initial_state(n),
+                                   np.zeros((1, 1)), 1, 1e-11, steps, stride)
+    assert_bit_equal(tr.states, want, "configs[4] n=1e4, 1e3 steps")
+
+
 def test_derivative_golden(sto):
     from paper_2312_01121_b200.backends.b200 import B200Backend
 

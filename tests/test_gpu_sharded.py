@@ -9,7 +9,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import assert_bit_equal
+from conftest import assert_bit_equal, fuzz_examples
 
 pytestmark = pytest.mark.gpu
 
@@ -164,7 +164,7 @@ from hypothesis import HealthCheck, given, settings  # noqa: E402
 from hypothesis import strategies as st  # noqa: E402
 
 
-@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow,
+@settings(max_examples=fuzz_examples(40), deadline=None, suppress_health_check=[HealthCheck.too_slow,
                                                                  HealthCheck.function_scoped_fixture])
 @given(n=st.integers(8, 2500), world=st.integers(2, 8), steps=st.integers(1, 30),
        sps=st.integers(1, 5), fam=st.sampled_from([0, 0x1, 0x2 | 0x8]),

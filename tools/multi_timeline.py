@@ -7,7 +7,8 @@ import ctypes, sys
 import numpy as np
 sys.path.insert(0, ".")
 import paper_2312_01121_b200._native as nat
-nat.LIB_PATH = nat.LIB_PATH.with_name("libsto_b200_timeline.so")
+import os
+nat.LIB_PATH = nat.LIB_PATH.with_name(os.environ.get("STO_TL_LIB", "libsto_b200_timeline.so"))
 import torch
 import paper_2312_01121_b200 as sto
 from paper_2312_01121_b200.sharding import _shard_plan, shard_rows
