@@ -668,8 +668,6 @@ int sto_plan_create(sto_plan **out, const sto_plan_desc *d) {
             }
         }
         P->grid = g;
-        if (P->rows_cap > P->chunk_cols)  // the row phase stages the x slice in the X window
-            return bail(fail(STO_E_PARAM, "sharded plan: more rows per CTA than the x window holds"));
     } else if (n <= 32 && !(fl & STO_PLAN_NO_TINY) && !forced) {
         P->kind = kTiny;
         P->grid = 1;
@@ -1255,7 +1253,7 @@ int sto_integrate_group(sto_plan **plans, int32_t world, const sto_run *r, sto_s
     p.rows_cap = cap;
     p.chunk_cols = P0->chunk_cols;
     const size_t smem = grid_smem(cap, P0->L.cs, p.chunk_cols, P0->kind == kResident);
-    if (smem > kSmemBudget || cap > p.chunk_cols)
+    if (smem > kSmemBudget)
         return fail(STO_E_PARAM, "group shard does not fit shared memory");
     p.mp.world = world;
     p.mp.rank_base = 0;

@@ -335,50 +335,8 @@ __global__ void __launch_bounds__(NT, 1) grid_rk4_kernel(const __grid_constant__
                                                              : p.m[3 * (size_t)k];
                         xs[col_perm(cs, k) - x_base] = v;
                     }
-                } else if constexpr (MULTI) {
-                    // the receive buffer is in LOGICAL order (each rank pushes its
-                    // contiguous row slice as 16-byte vectors); the physical window
-                    // [x_base, x_base + x_len) holds exactly the logical columns of the
-                    // same range (segments are contiguous), permuted.  Walk it in
-                    // PHYSICAL order, one 16-byte slot per thread (conflict-free shared
-                    // stores): slot m of a segment of C columns per lane holds the
-                    // logical pair base + (m & 31) * C + 2 (m >> 5), +1; +0.0 for k >= n
-                    const double *src = xrecv + (size_t)((p.mp.epoch_base + e) & 1) * cs.ldw;
-                    const int full_end = cs.nfull * kSegFull;
-                    auto logical_of = [&](int pos) {  // first logical column of physical pair slot pos
-                        int base = pos & ~(kSegFull - 1), c = 16;
-                        if (pos >= full_end) {
-                            int t = cs.ntail - 1;
-                            while (t > 0 && pos < cs.tail_base[t]) --t;
-                            base = cs.tail_base[t];
-                            c = cs.tail_c[t];
-                        }
-                        const int mi = (pos - base) >> 1;
-                        return base + (mi & 31) * c + 2 * (mi >> 5);
-                    };
-                    // four independent L2 loads in flight per thread before the stores
-                    constexpr int kU = 4;
-                    const int npairs = x_len / 2;
-                    for (int i0 = threadIdx.x; i0 < npairs; i0 += kU * blockDim.x) {
-                        double2 v[kU];
-#pragma unroll
-                        for (int u = 0; u < kU; ++u) {
-                            const int i = i0 + u * blockDim.x;
-                            v[u] = make_double2(0.0, 0.0);
-                            if (i < npairs) {
-                                const int k = logical_of(x_base + 2 * i);
-                                if (k + 1 < cs.n) v[u] = __ldcg(reinterpret_cast<const double2 *>(src + k));
-                                else if (k < cs.n) v[u].x = __ldcg(src + k);
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < kU; ++u) {
-                            const int i = i0 + u * blockDim.x;
-                            if (i < npairs) reinterpret_cast<double2 *>(xs)[i] = v[u];
-                        }
-                    }
                 } else {
-                    const double *src = xrecv + (size_t)(e & 1) * cs.ldw + x_base;
+                    const double *src = xrecv + (size_t)((MULTI ? p.mp.epoch_base + e : e) & 1) * cs.ldw + x_base;
                     const double2 *src2 = reinterpret_cast<const double2 *>(src);
                     double2 *dst2 = reinterpret_cast<double2 *>(xs);
 #pragma unroll 4
@@ -469,34 +427,13 @@ __global__ void __launch_bounds__(NT, 1) grid_rk4_kernel(const __grid_constant__
                 }
             }
             if constexpr (MULTI) {
-                xs[r] = xpub;  // staged: the X window is free during the row phase
+                // this row's x into every rank's receive buffer (physical layout, so
+                // the receivers stage it exactly like the unsharded kernel; one
+                // 8-byte store per row and peer -- 80 KB per stage at N = 1e4)
+                const int pos = col_perm(cs, k);
+                for (int q = 0; q < p.mp.world; ++q) p.mp.xbuf_of[q][par_next + pos] = xpub;
             } else {
                 xnext[col_perm(cs, k)] = xpub;
-            }
-        }
-        if constexpr (MULTI) {
-            // push this CTA's contiguous slice [k0, k0 + nrow) of the stage x into
-            // every rank's receive buffer (logical order) as 16-byte stores: one
-            // scalar head when k0 is odd, pairs, one scalar tail -- instead of
-            // nrow scattered 8-byte stores per peer
-            __syncthreads();
-            if (integrate) {
-                const long long k0 = rb + r0;
-                const int head = (int)(k0 & 1) < nrow ? (int)(k0 & 1) : 0;
-                const int npair = (nrow - head) >> 1;
-                const int per = head + npair + ((nrow - head) & 1);
-                for (int i = threadIdx.x; i < per * p.mp.world; i += blockDim.x) {
-                    const int q = i / per, j = i - q * per;
-                    double *dst = p.mp.xbuf_of[q] + par_next + k0;
-                    if (j < head) {
-                        dst[0] = xs[0];
-                    } else if (j < head + npair) {
-                        const int o = head + 2 * (j - head);
-                        *reinterpret_cast<double2 *>(dst + o) = make_double2(xs[o], xs[o + 1]);
-                    } else {
-                        dst[nrow - 1] = xs[nrow - 1];
-                    }
-                }
             }
         }
         GTL(e, 3);
