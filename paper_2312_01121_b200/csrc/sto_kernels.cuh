@@ -483,6 +483,11 @@ __global__ void __launch_bounds__(NT, 1) grid_rk4_kernel(const __grid_constant__
 // n <= 32: one warp, everything in registers; shared memory only carries the
 // published stage x between lanes.  NMAX = smallest power of two >= n.
 // ----------------------------------------------------------------------------
+#ifndef STO_TINY_GROUP
+#define STO_TINY_GROUP 4
+#endif
+constexpr int kTinyGroup = STO_TINY_GROUP;  // RK4 steps per speculative-division proof check
+
 template <int NMAX>
 __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__ KParams p) {
     __shared__ double xsh[NMAX > 1 ? NMAX : 1];
@@ -567,19 +572,29 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
         const V3 k4 = row_rhs<S>(s, coupling(s.x), cin, c, ok);
         return rk4_final(m, acc, k3, k4, p.dt6);
     };
-    auto rk4 = [&]() {
+    // kG steps per proof check: the branch on the proofs (and, for n > 1, the
+    // warp vote) is paid once per group; a failed proof replays the group
+    // from its saved start state with the library division.
+    auto rk4_group = [&](auto group) {
+        constexpr int kG = decltype(group)::value;
+        const V3 m_save = m;
         bool ok = true;
-        const V3 m1 = rk4_body(std::true_type{}, &ok);
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+            m = rk4_body(std::true_type{}, &ok);
+            publish(m.x);
+        }
         bool replay;
         if constexpr (NMAX == 1) replay = !ok;
         else replay = __any_sync(0xffffffffu, live && !ok);
         if (replay) {
+            m = m_save;
             publish(m.x);  // the stage x of the failed attempt are in xsh
-            m = rk4_body(std::false_type{}, nullptr);
-        } else {
-            m = m1;
+            for (int g = 0; g < kG; ++g) {
+                m = rk4_body(std::false_type{}, nullptr);
+                publish(m.x);
+            }
         }
-        publish(m.x);
     };
     long long step = 0;
     while (step < p.steps) {
@@ -588,7 +603,9 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
             const long long hold_end = (step / p.sps + 1) * p.sps;
             if (hold_end < seg_end) seg_end = hold_end;
         }
-        for (long long i = step; i < seg_end; ++i) rk4();
+        long long i = step;
+        for (; i + kTinyGroup <= seg_end; i += kTinyGroup) rk4_group(std::integral_constant<int, kTinyGroup>{});
+        for (; i < seg_end; ++i) rk4_group(std::integral_constant<int, 1>{});
         step = seg_end;
         if (step == next_rec || step == p.steps) {
             const long long rec = (step == next_rec) ? rec_idx : p.n_records - 1;
