@@ -85,10 +85,11 @@ def env_rank():
 # Dependent fp64 chain of one RK4 step in the pinned order (sto_device.cuh): 15
 # dependent DMUL/DADD between two h_s divisions in stages 1-3 (m.p, 1 + lam*md,
 # then h_s*q_z -> b_z -> a_y -> e_x -> dm/dt -> stage point) and 17 around the
-# RK4 combination, i.e. 62 x 8.4 cycles, plus 4 speculative divisions at 74.25
-# cycles (tools/microbench.cu, profiles/r02c_microbench.json: dadd 8.44, dmul
-# 8.38, ddiv_spec 74.25; __ddiv_rn was 113.5) = 818 cycles.
-RK4_CHAIN_CYCLES = 62 * 8.4 + 4 * 74.25
+# RK4 combination, i.e. 62 x 8.4 cycles, plus 4 speculative divisions at 68.5
+# cycles (tools/microbench.cu: dadd 8.44, dmul 8.38, ddiv_spec 68.5 with the
+# four-DFMA quotient, profiles/r02k_division_variants.txt; __ddiv_rn was 113.5)
+# = 795 cycles.
+RK4_CHAIN_CYCLES = 62 * 8.4 + 4 * 68.5
 
 
 def measured_peaks() -> dict:

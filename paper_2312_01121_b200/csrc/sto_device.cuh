@@ -32,8 +32,8 @@ __device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a,
 // __ddiv_rn costs ~113 cycles of dependent latency (profiles/r01_microbench.json),
 // most of it the MUFU seed, three Newton/FMA corrections and a range test whose
 // branch sits in front of every consumer.  Here the quotient comes from a
-// shorter chain (seed -> e -> e+e^2 -> q0 -> remainder -> q: the seed plus
-// five DFMA) and its correctness is *proved* afterwards, off the chain:
+// shorter chain (seed -> e -> q0 = a r0 (1 + e) -> remainder -> q: the seed
+// plus four DFMA) and its correctness is *proved* afterwards, off the chain:
 //   * q == RN(a/b) iff |a/b - q| < half the spacing of doubles on a/b's side
 //     of q, i.e. |a - b*q| < |b| * ulp(q)/2 (ulp(q)/4 when q is a power of two,
 //     conservatively, so the narrower gap below 2^k is used on both sides);
@@ -44,19 +44,33 @@ __device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a,
 //     a q off by more fails the test by a wide margin either way;
 //   * the exponent guards keep every quantity above (q, b, b*ulp/2, the
 //     remainder) normal and finite; outside them, or for NaN/inf/0, ok = false.
-// The caller must redo the work with rdiv() when ok is false (the kernels
-// replay the whole RK4 step; in practice it never triggers, see
-// sto_selftest_div).  IEEE division is unique, so the bits equal __ddiv_rn's.
+// The caller must redo the work with rdiv() when ok is false (the tiny kernel
+// replays its group of RK4 steps; ~3e-4 of the quotients, see sto_selftest_div).
+// IEEE division is unique, so the bits equal __ddiv_rn's.
+// STO_DIV_SHORT (default): seed + FOUR DFMA (one correction with the seed
+// itself); ~3e-4 of the quotients miss the last bit and fail the proof (replayed).
+// 0: seed + five DFMA (a refined reciprocal), every RHS-domain quotient proved.
+// N = 1: 2.44e6 vs 2.39e6 RK4 steps/s (profiles/r02k_division_variants.txt).
+#ifndef STO_DIV_SHORT
+#define STO_DIV_SHORT 1
+#endif
 __device__ __forceinline__ double rdiv_spec(double a, double b, bool &ok) {
     double r0;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(b));
     const double e = __fma_rn(-b, r0, 1.0);
     const double ar0 = __dmul_rn(a, r0);
+#if STO_DIV_SHORT
+    // seed + four DFMA: q0 = a r0 (1 + e), one correction with the seed itself
+    const double q0 = __fma_rn(ar0, e, ar0);
+    const double rem = __fma_rn(-b, q0, a);
+    const double q = __fma_rn(rem, r0, q0);
+#else
     const double pe = __fma_rn(e, e, e);
     const double y = __fma_rn(r0, pe, r0);
     const double q0 = __fma_rn(ar0, pe, ar0);
     const double rem = __fma_rn(-b, q0, a);
     const double q = __fma_rn(rem, y, q0);
+#endif
     // ---- proof of correct rounding (independent of the chain above) ----
     const double rem2 = __fma_rn(-b, q, a);
     const long long qb = __double_as_longlong(q);
