@@ -108,6 +108,38 @@ def test_reference_bench_lists_b200(plugged, capsys):
     assert "gpu n=100:" in out
 
 
+@pytest.mark.gpu
+def test_reference_simulate_csv_byte_identical(plugged, tmp_path, capsys):
+    """`spinosc simulate --backend gpu --output x.csv` (cli.py:171-187) through the
+    whole-run hook: the trajectory CSV equals the one the reference's own
+    `fused` backend writes for the same run, byte for byte."""
+    import spinosc.cli as cli
+
+    args = ["simulate", "--n", "60", "--steps", "400", "--record-stride", "40", "--seed", "3"]
+    rc_gpu = cli.main(args + ["--backend", "gpu", "--output", str(tmp_path / "gpu.csv")])
+    rc_ref = cli.main(args + ["--backend", "fused", "--output", str(tmp_path / "fused.csv")])
+    out = capsys.readouterr().out
+    assert rc_gpu == 0 and rc_ref == 0, out
+    assert (tmp_path / "gpu.csv").read_bytes() == (tmp_path / "fused.csv").read_bytes()
+    assert "backend=gpu n=60" in out
+
+
+@pytest.mark.gpu
+def test_reference_scaling_command_runs_b200(plugged, tmp_path, capsys):
+    """`spinosc scaling --backend gpu` (cli.py:284-313): the reference's
+    derivative-cost sweep times the B200 K0 derivative and fits an exponent
+    (its fit needs four sizes spanning a decade, bench.py:233-239)."""
+    import spinosc.cli as cli
+
+    out_csv = tmp_path / "scaling.csv"
+    rc = cli.main(["scaling", "--backend", "gpu", "--n-list", "100,300,1000,3000", "--evals", "3",
+                   "--output", str(out_csv)])
+    out = capsys.readouterr().out
+    assert rc == 0, out
+    assert "fitted scaling exponent" in out
+    assert out_csv.read_text().splitlines()[0] == "n,seconds"
+
+
 def test_elementwise_field_helpers_match_reference(plugged):
     """effective_field / spin_torque_strength: same operations as ref model.py:152-173."""
     import paper_2312_01121_b200 as sto
