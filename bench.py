@@ -406,7 +406,7 @@ def run_ours_ensemble(args, rank, world, local_rank):
             "gpu_launches": 2 * args.steps,
             "roofline": ({"bound": "fp64", "achieved": achieved, "peak": FP64_MULADD_PEAK_TFLOPS,
                           "unit": "TFLOP/s", "frac": achieved / FP64_MULADD_PEAK_TFLOPS,
-                          "traffic": None,
+                          "traffic": traffic_per_launch("ens512_exact", steps),
                           "peak_source": "FP64 CUDA-core mul/add issue rate: half the measured DFMA "
                                          "34.0 TFLOP/s (tools/fp64_peak.cu); the pinned order forbids FMA",
                           "kernel": "ens_exact_kernel"} if exact else

@@ -13,4 +13,5 @@ run n1000 2000 reg_rk4
 run ens512 200 ens_rk4
 run n100 2000 clu_
 run n1 20000 tiny_rk4
+run ens512_exact 40 ens_exact
 ls -la gpurun_out/traffic_*.csv
