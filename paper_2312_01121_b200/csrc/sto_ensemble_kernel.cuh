@@ -85,12 +85,20 @@ constexpr int kEnsTmemCols = 512;               // whole TMEM: 128 lanes x 512 x
 constexpr int kEnsEpiUnroll = STO_ENS_EPI_UNROLL;  // epilogue outputs in flight per thread
 constexpr int kEnsTmemOut = 18;                 // columns per output: m, acc, s (3 doubles each)
 constexpr int kEnsKAlign = 8;                   // K padded to 8: chunk bytes % 16 == 0, even k-steps
+#ifndef STO_ENS_ALTERNATE
+#define STO_ENS_ALTERNATE 0
+#endif
+// 1: the two groups' GEMMs take turns (measured 2.81e9 vs 3.34e9 osc-steps/s free
+// running: a lone 8-warp group reaches only ~0.6 of the DMMA peak inside the
+// kernel, so the groups must overlap in the GEMM to fill the pipe; A/B only)
+constexpr bool kEnsAlternate = STO_ENS_ALTERNATE;
 
 __host__ __device__ constexpr int ens_slot_doubles(int u) { return 8 * u * kEnsKC + kEnsKC * kEnsGW; }
 __host__ __device__ constexpr size_t ens_smem_bytes(int u) {
     return sizeof(double) * ((size_t)kEnsGroups * kEnsSlots * ens_slot_doubles(u) + 8 * u * kEnsLDB +
                              kEnsBT * 11 + 8 * u) +
-           sizeof(unsigned long long) * 2 * kEnsGroups * kEnsSlots + 16;  // barriers, counters, TMEM base, gate, stop[2]
+           sizeof(unsigned long long) * (2 * kEnsGroups * kEnsSlots + kEnsGroups) +
+           24;  // ring barriers, GEMM-turn barriers, counters, TMEM base, gate, stop[2], exited[2]
 }
 static_assert(ens_smem_bytes(kEnsMaxU) <= 227 * 1024, "ensemble shared memory budget");
 
@@ -155,6 +163,17 @@ __device__ __forceinline__ bool mbar_test(unsigned long long *b, uint32_t parity
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long *b, uint32_t parity) {  // blocks up to a HW time limit
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n}"
         : "=r"(ok)
         : "r"(smem_u32(b)), "r"(parity)
@@ -282,10 +301,12 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
     double *cs = cpb + TR * kEnsLDB;                   // [64][11] member consts
     double *wins = cs + kEnsBT * 11;                   // [TR] input weights of the tile's rows (n_in = 1)
     unsigned long long *full_all = reinterpret_cast<unsigned long long *>(wins + TR);
-    unsigned *done_all = reinterpret_cast<unsigned *>(full_all + kEnsGroups * kEnsSlots);
+    unsigned long long *gemm_done = full_all + kEnsGroups * kEnsSlots;  // [2] GEMM turns (see below)
+    unsigned *done_all = reinterpret_cast<unsigned *>(gemm_done + kEnsGroups);
     uint32_t *tmem_base_slot = done_all + kEnsGroups * kEnsSlots;
     volatile int *go = reinterpret_cast<volatile int *>(tmem_base_slot + 1);  // group 1 start gate
     volatile int *stop_grp = go + 1;  // [2] per group: stop after this recording step
+    volatile int *exited = stop_grp + 2;  // [2] per group: left the stage loop (no more turns)
 
     const int rt = blockIdx.x % p.n_rt, ct = blockIdx.x / p.n_rt;  // row tile, member column
     const int row0 = rt * TR, col0 = ct * kEnsBT;
@@ -313,6 +334,10 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
         for (int s = 0; s < kEnsGroups * kEnsSlots; ++s) {
             mbar_init(&full_all[s], 1);
             done_all[s] = 0u;
+        }
+        for (int g = 0; g < kEnsGroups; ++g) {
+            mbar_init(&gemm_done[g], kEnsGroupThreads / 32);
+            exited[g] = 0;
         }
         *go = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -437,6 +462,20 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
 #ifdef STO_TIMELINE
             long long waited = 0;
 #endif
+            // GEMM turns: the two groups' K loops alternate -- group 1 runs its
+            // stage-g GEMM after group 0's, group 0 its stage-g GEMM after group
+            // 1's stage g-1 -- so each GEMM has the DMMA pipe to itself while the
+            // other group is in its epilogue and exchange (left free, the two
+            // groups drift into phase and share the pipe, then idle together).
+            // A group can run at most one turn ahead, so mbarrier parity is
+            // unambiguous; a group that has left the loop (record-step stop)
+            // takes no more turns.
+            if (kEnsAlternate && !p.debug_solo && (grp == 1 || gstage > 0)) {
+                const int other = grp ^ 1;
+                const uint32_t par = (uint32_t)((grp == 1 ? gstage : gstage - 1) & 1);
+                while (!mbar_try(&gemm_done[other], par) && !exited[other]) {
+                }
+            }
             for (int ch = 0; ch < n_chunks; ++ch) {
 #ifdef STO_TIMELINE
                 const long long w0 = clock64();
@@ -500,6 +539,10 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
                     slot = 0;
                     phase ^= 1;
                 }
+            }
+            if (kEnsAlternate) {  // this group's GEMM turn is over
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&gemm_done[grp]);
             }
             // ---- split-K reduction into cpb[row][member] --------------------
             double *cpg = cpb + kEnsGW * grp + 8 * mu + 2 * t4;
@@ -646,6 +689,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
         }
     }
 done:
+    if (lane == 0 && wl == 0) exited[grp] = 1;  // the other group takes no more turns after this one
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
