@@ -92,6 +92,12 @@ constexpr int kEnsKAlign = 8;                   // K padded to 8: chunk bytes % 
 // running: a lone 8-warp group reaches only ~0.6 of the DMMA peak inside the
 // kernel, so the groups must overlap in the GEMM to fill the pipe; A/B only)
 constexpr bool kEnsAlternate = STO_ENS_ALTERNATE;
+// GEMM warp tile: 1 = U x 1 DMMA tiles, split-K 2 (warp = member unit x k-step
+// parity); 2 = U x 2 tiles (two member units share each A fragment), split-K 4
+#ifndef STO_ENS_NT
+#define STO_ENS_NT 1
+#endif
+constexpr int kEnsNT = STO_ENS_NT;
 
 __host__ __device__ constexpr int ens_slot_doubles(int u) { return 8 * u * kEnsKC + kEnsKC * kEnsGW; }
 __host__ __device__ constexpr size_t ens_smem_bytes(int u) {
@@ -456,9 +462,11 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
         for (int stage = 0; stage < 4; ++stage, ++gstage) {  // unrolled: stage branches resolve at compile time
             ENS_TL(gstage, 0);
             const double u1 = (p.n_in == 1) ? samp[(size_t)sidx] : 0.0;  // lands during the GEMM
-            double acc[U][2];
+            double acc[U][kEnsNT][2];
 #pragma unroll
-            for (int r = 0; r < U; ++r) acc[r][0] = acc[r][1] = 0.0;
+            for (int r = 0; r < U; ++r)
+#pragma unroll
+                for (int j = 0; j < kEnsNT; ++j) acc[r][j][0] = acc[r][j][1] = 0.0;
 #ifdef STO_TIMELINE
             long long waited = 0;
 #endif
@@ -487,7 +495,29 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
                 const double *W = ring + slot * SS;
                 const double *X = W + WS;
                 const int nk = kc_of(ch) >> 2;  // k-steps in this chunk (even)
-                if (nk == kEnsKC / 4) {
+                if constexpr (kEnsNT == 2) {
+                    // warp = member-unit pair x k-step phase (mod 4); one A fragment feeds
+                    // two DMMAs
+                    const int pair = wl & 1, kq = wl >> 1;
+                    auto kstep = [&](int kk, int nkk) {
+                        double a[U];
+#pragma unroll
+                        for (int r = 0; r < U; ++r) a[r] = W[(r * nkk + kk) * 32 + lane];
+                        const double b0 = X[(kk * 4 + 2 * pair) * 32 + lane];
+                        const double b1 = X[(kk * 4 + 2 * pair + 1) * 32 + lane];
+#pragma unroll
+                        for (int r = 0; r < U; ++r) {
+                            dmma(acc[r][0][0], acc[r][0][1], a[r], b0);
+                            dmma(acc[r][kEnsNT - 1][0], acc[r][kEnsNT - 1][1], a[r], b1);
+                        }
+                    };
+                    if (nk == kEnsKC / 4) {
+#pragma unroll
+                        for (int q = 0; q < kEnsKC / 16; ++q) kstep(kq + 4 * q, kEnsKC / 4);
+                    } else {
+                        for (int kk = kq; kk < nk; kk += 4) kstep(kk, nk);
+                    }
+                } else if (nk == kEnsKC / 4) {
                     // full chunk: compile-time offsets, fragments of the next k-step loaded
                     // while the DMMAs of this one issue (register double buffer)
                     constexpr int NQ = kEnsKC / 8;  // k-steps of this warp's parity
@@ -504,7 +534,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
                             bf[(q + 1) & 1] = X[(kn * 4 + mu) * 32 + lane];
                         }
 #pragma unroll
-                        for (int r = 0; r < U; ++r) dmma(acc[r][0], acc[r][1], a[q & 1][r], bf[q & 1]);
+                        for (int r = 0; r < U; ++r) dmma(acc[r][0][0], acc[r][0][1], a[q & 1][r], bf[q & 1]);
                     }
                 } else {
                     for (int kk = kph; kk < nk; kk += 2) {
@@ -513,7 +543,7 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
                         for (int r = 0; r < U; ++r) a[r] = W[(r * nk + kk) * 32 + lane];
                         const double bf = X[(kk * 4 + mu) * 32 + lane];
 #pragma unroll
-                        for (int r = 0; r < U; ++r) dmma(acc[r][0], acc[r][1], a[r], bf);
+                        for (int r = 0; r < U; ++r) dmma(acc[r][0][0], acc[r][0][1], a[r], bf);
                     }
                 }
                 // Slot consumed by this warp; the LAST of the group's warps to get here
@@ -545,13 +575,38 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
                 if (lane == 0) mbar_arrive(&gemm_done[grp]);
             }
             // ---- split-K reduction into cpb[row][member] --------------------
+            if constexpr (kEnsNT == 2) {
+                // four k-step phases accumulate in turn (the last one stores first)
+                const int pair = wl & 1, kq = wl >> 1;
+#pragma unroll
+                for (int round = 3; round >= 0; --round) {
+                    if (kq == round) {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            double *cpg = cpb + kEnsGW * grp + 8 * (2 * pair + j) + 2 * t4;
+#pragma unroll
+                            for (int r = 0; r < U; ++r) {
+                                double *d = cpg + (8 * r + g8) * kEnsLDB;
+                                if (round == 3) {
+                                    d[0] = acc[r][j][0];
+                                    d[1] = acc[r][j][1];
+                                } else {
+                                    d[0] = acc[r][j][0] + d[0];
+                                    d[1] = acc[r][j][1] + d[1];
+                                }
+                            }
+                        }
+                    }
+                    group_sync(grp);
+                }
+            } else {
             double *cpg = cpb + kEnsGW * grp + 8 * mu + 2 * t4;
             if (kph == 1) {
 #pragma unroll
                 for (int r = 0; r < U; ++r) {
                     double *d = cpg + (8 * r + g8) * kEnsLDB;
-                    d[0] = acc[r][0];
-                    d[1] = acc[r][1];
+                    d[0] = acc[r][0][0];
+                    d[1] = acc[r][0][1];
                 }
             }
             group_sync(grp);
@@ -559,11 +614,12 @@ __global__ void __launch_bounds__(kEnsThreads, 1) ens_rk4_kernel(const __grid_co
 #pragma unroll
                 for (int r = 0; r < U; ++r) {
                     double *d = cpg + (8 * r + g8) * kEnsLDB;
-                    d[0] = acc[r][0] + d[0];
-                    d[1] = acc[r][1] + d[1];
+                    d[0] = acc[r][0][0] + d[0];
+                    d[1] = acc[r][0][1] + d[1];
                 }
             }
             group_sync(grp);
+            }
             ENS_TL(gstage, 1);
 #ifdef STO_TIMELINE
             if (blockIdx.x == 0 && threadIdx.x % kEnsGroupThreads == 0 && gstage >= 40 && gstage < 56)
