@@ -165,7 +165,8 @@ def shard_members(batch: int, world: int, rank: int) -> np.ndarray:
 
 
 def integrate_ensemble_sharded(backend, consts: np.ndarray, samples: np.ndarray,
-                               steps_per_sample: int, config, group, exact: bool = False) -> np.ndarray:
+                               steps_per_sample: int, config, group, exact: bool = False,
+                               m0: np.ndarray | None = None) -> np.ndarray:
     """Batch-sharded ensemble: this rank's members on its own
     GPU, then one all-gather of the recorded grids.  consts (B, 11) and
     samples ([B,] n_samples, n_in) describe the WHOLE batch; returns the
@@ -182,7 +183,10 @@ def integrate_ensemble_sharded(backend, consts: np.ndarray, samples: np.ndarray,
     mine = shard_members(batch, world, rank)
     counts = [(0, len(shard_members(batch, world, r))) for r in range(world)]
     samples_mine = samples[mine] if samples.ndim == 3 else samples
-    m = np.tile(initial_state(config.n, config.phi0)[None], (len(mine), 1, 1))
+    if m0 is None:
+        m = np.tile(initial_state(config.n, config.phi0)[None], (len(mine), 1, 1))
+    else:
+        m = np.ascontiguousarray(m0[mine])
     local_error = None
     states = None
     try:

@@ -110,6 +110,27 @@ def test_several_launches(sto, oracle_mod, monkeypatch):
     _check(sto, oracle_mod, top, _sweep(sto, batch), cfg, (0, 63, 64, 127, 128, 149))
 
 
+def test_custom_initial_states_bit_exact(sto, oracle_mod):
+    """integrate_ensemble(m0=...) with one random unit-norm start per member:
+    each member equals the oracle run from that start (the f4 extension of
+    integrate(m0=) carried to ensembles)."""
+    n, batch, steps = 70, 5, 80
+    top = _rand_top(sto, n, seed=21)
+    g = np.random.default_rng(22)
+    m0 = g.normal(size=(batch, n, 3))
+    m0 /= np.linalg.norm(m0, axis=2, keepdims=True)
+    params = _sweep(sto, batch)
+    cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=20)
+    ens = sto.integrate_ensemble(top, params, cfg, exact=True, m0=m0)
+    for b in range(batch):
+        want, _ = oracle_mod.integrate(top.coupling.entries, top.input_weights.entries,
+                                       sto.kernel_scalars(params[b]), m0[b], np.zeros((1, 1)), 1,
+                                       1e-11, steps, 20)
+        assert_bit_equal(ens.states[:, b], want, f"member {b}")
+    with pytest.raises(sto.ParameterError):
+        sto.integrate_ensemble(top, params, cfg, m0=m0[:, :10])
+
+
 def test_matches_dmma_path_within_tolerance(sto):
     n, batch = 200, 64
     top = sto.build_topology(n, seed=4)
