@@ -1394,6 +1394,10 @@ STO_API int sto_debug_grid_timeline(unsigned long long *out, int count) {
     STO_CUDA(cudaMemcpyFromSymbol(out, g_grid_timeline, sizeof(unsigned long long) * count));
     return STO_OK;
 }
+STO_API int sto_debug_multi_timeline(unsigned long long *out, int count) {
+    STO_CUDA(cudaMemcpyFromSymbol(out, g_multi_timeline, sizeof(unsigned long long) * count));
+    return STO_OK;
+}
 STO_API int sto_debug_timeline(unsigned long long *out, int count) {
     STO_CUDA(cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * count));
     return STO_OK;

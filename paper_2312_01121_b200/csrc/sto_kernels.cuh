@@ -136,23 +136,40 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long
     __syncthreads();
 }
 
+#ifdef STO_TIMELINE
+// debug build (tools/multi_timeline.py): clock64 stamps of rank 0's CTA 0 inside
+// multi_sync for exchanges [100, 116): 0 entry, 1 own fence done, 2 local counter
+// complete, 3 all flags seen, 4 exit
+__device__ unsigned long long g_multi_timeline[16][5];
+#define MTL(ev)                                                                         \
+    do {                                                                                \
+        if (tl_slot >= 0) g_multi_timeline[tl_slot][ev] = clock64();                    \
+    } while (0)
+#else
+#define MTL(ev)
+#endif
+
 // local counter barrier, then epoch flags across ranks (see MultiParams)
 __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInfo &sh, int rank,
                                            int lcta, unsigned long long local_target,
                                            unsigned long long epoch, bool record_stage,
-                                           const StatusDev *status, volatile int *sflag) {
+                                           const StatusDev *status, volatile int *sflag,
+                                           int tl_slot = -1) {
     // One system-scope fence per role (each costs a round to the peers): the CTA's
     // release of its peer stores, the leader's release of its flags (then plain
     // relaxed stores), and ONE acquire after thread 0 has seen every flag.
     __syncthreads();
     if (threadIdx.x == 0) {
+        MTL(0);
         asm volatile("fence.acq_rel." STO_MULTI_SCOPE ";" ::: "memory");  // our peer stores are system-visible
+        MTL(1);
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(sh.bar) : "memory");
         unsigned long long v;
         do {
             asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(sh.bar) : "memory");
         } while (v < local_target);
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        MTL(2);
         if (lcta == 0) {
             // every local CTA has passed the barrier, so a divergence on this
             // recording step is already in the (local) status
@@ -199,7 +216,9 @@ __device__ __forceinline__ bool multi_sync(const MultiParams &mp, const ShardInf
                 }
             }
         }
+        MTL(3);
         asm volatile("fence.acq_rel." STO_MULTI_SCOPE ";" ::: "memory");  // acquire: every peer's x is visible
+        MTL(4);
         if (stop) *sflag = 1;
     }
     __syncthreads();
@@ -447,7 +466,8 @@ __global__ void __launch_bounds__(NT, 1) grid_rk4_kernel(const __grid_constant__
             if (*sflag) break;
         } else if constexpr (MULTI) {
             if (multi_sync(p.mp, sh, rank, b, (unsigned long long)(e + 1) * G,
-                           p.mp.epoch_base + e + 1, stage == 3 && rec >= 0, p.status, sflag) ||
+                           p.mp.epoch_base + e + 1, stage == 3 && rec >= 0, p.status, sflag,
+                           (blockIdx.x == 0 && e >= 100 && e < 116) ? (int)(e - 100) : -1) ||
                 e + 1 == total_stages)
                 break;
         } else {

@@ -43,3 +43,10 @@ for s in range(15):
           f"total {t[s+1,0]-t[s,0]:7.0f} cyc")
 med = np.median(np.array(rows), axis=0)
 print(f"median: x-stage {med[0]:.0f} block {med[1]:.0f} rows {med[2]:.0f} exchange {med[3]:.0f} total {med[4]:.0f} cyc")
+if world > 1:
+    mb = (ctypes.c_ulonglong * 80)()
+    L.sto_debug_multi_timeline(mb, 80)
+    mt = np.array(mb, dtype=np.float64).reshape(16, 5)
+    d = np.median(np.diff(mt[:15], axis=1), axis=0)
+    print(f"multi_sync median: own fence {d[0]:.0f}  local barrier {d[1]:.0f}  flags {d[2]:.0f}  "
+          f"acquire fence {d[3]:.0f} cyc")
