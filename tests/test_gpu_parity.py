@@ -140,6 +140,22 @@ def test_benched_config4_full_horizon_bit_exact(sto, oracle_mod):
     assert_bit_equal(tr.states, want, "configs[4] n=1e4, 1e3 steps")
 
 
+def test_benched_n4e4_full_horizon_bit_exact(sto, oracle_mod):
+    """configs[4] upper end as benched (bench.py n4e4): N = 4e4, device-built
+    seed-0 reservoir, 50 RK4 steps -- the chunked-x streaming kernel over the
+    whole benched horizon, every 10th state bit-identical to the oracle
+    (~45 s of 16-thread oracle time)."""
+    n, steps, stride = 40_000, 50, 10
+    top = sto.build_topology_device(n, seed=0)
+    params = sto.PhysicalParams()
+    cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=stride)
+    tr = sto.integrate(top, params, cfg)
+    want, _ = oracle_mod.integrate(top.coupling.entries, top.input_weights.entries,
+                                   sto.kernel_scalars(params), sto.initial_state(n),
+                                   np.zeros((1, 1)), 1, 1e-11, steps, stride)
+    assert_bit_equal(tr.states, want, "configs[4] n=4e4, 50 steps")
+
+
 def test_derivative_golden(sto):
     from paper_2312_01121_b200.backends.b200 import B200Backend
 
