@@ -16,18 +16,22 @@
 // stage_point / acc_k2 / rk4_final of the single-trajectory kernels.
 //
 // Structure (one persistent cooperative launch per run):
-//  * Tiles of 32 oscillators x 64 members; CTA c owns tiles c, c + G, ... and
-//    processes them in that order every stage (G = grid, one CTA per SM).
-//  * A CTA tile is 8 warps of 8 x 32 outputs (warp row group wr, member half
-//    wb); lane (lr, lb) owns 2 oscillators x 4 members: rows 8wr + lr + 4i,
-//    members 32wb + 16j + 2lb + e.  Lanes with the same lr read the same W
-//    words (broadcast) and lanes with the same lb the same x words, so each
-//    4-column step loads 12 16-byte words per lane for 64 FP64 ops.
-//  * K streams in 32-column chunks (one leaf) through a 3-deep cp.async ring
-//    of [32 rows x 34] W (row pitch 34: conflict-free 16-byte row reads) and
-//    [32 cols x 64 members] x; the leaf-level stack lives in shared memory
-//    ([level][output][thread], conflict-free), the within-leaf nodes in
-//    registers (unrolled: three live nodes per output).
+//  * Tiles of TR = 8U oscillators x TB = 32 BV members (the host picks U so the
+//    tiles fill the SMs: N = 1000, B = 512 -> U = 7, BV = 2: 144 tiles of
+//    56 x 64); CTA c owns tiles c, c + G, ... and processes them in that order
+//    every stage (G = grid, one CTA per SM).
+//  * 8 warps; lane (lr = lane & 7, lb = lane >> 3) of warp w owns U
+//    oscillators x BV members: rows lr + 8i, members 4BV w + BV lb + e.
+//    Lanes with the same lr read the same W words (broadcast) and lanes with
+//    the same lb the same x words: a 4-column step loads 2U + 4 16-byte words
+//    (BV = 2) per lane for 16U FP64 ops, conflict-free.
+//  * K streams in 32-column chunks through a 2-deep cp.async ring of
+//    [TR rows x 34] W (row pitch 34: conflict-free 16-byte row reads) and
+//    [32 cols x TB members] x.  A leaf is 64 columns (two chunks): the
+//    within-chunk tree is unrolled in registers (three live nodes per
+//    output), the first chunk's node waits in a register for the second, and
+//    the leaf-level stack lives in shared memory ([level][output][thread],
+//    conflict-free).
 //  * RK state (m, stage point, acc, k3; the exact order needs k3 kept apart)
 //    in global planes [12][np][bp] (coalesced: consecutive lanes hold
 //    consecutive member pairs).
