@@ -56,7 +56,8 @@ enum KernelMode : int { kIntegrate = 0, kDerivative = 1, kMatvec = 2 };
 // pointers: CUDA-IPC-mapped NVLink memory on a multi-GPU box, or plain device
 // buffers when several logical ranks share one GPU for testing), then
 //   local barrier (counter) -> leader raises its epoch flag in every rank's
-//   flag array (st.release.sys) -> all CTAs wait for all `world` flags.
+//   flag array (one system-scope release fence, then relaxed stores) -> thread 0
+//   of every CTA polls all `world` flags and takes one system-scope acquire.
 // Epochs are 64-bit and monotonic across launches, so flags are never reset
 // while a peer may be writing them.
 // ----------------------------------------------------------------------------
