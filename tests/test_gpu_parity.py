@@ -408,3 +408,34 @@ def test_full_horizon_configs(sto, name, families):
     for fam in families[1:]:
         states, _, info = _run(sto, dd, fam)
         assert_bit_equal(states, d["states"], f"{name} [{fam}: {info['kernel_name']}]")
+
+
+@pytest.mark.parametrize("family", ["tiny", "cluster", "reg", "stream", "resident", "single"])
+def test_runs_are_deterministic_and_stateless(sto, family):
+    """SURVEY §5's determinism plan (the reference's thread-count / no-hidden-
+    state tests, test_backends.py:104-135): the same run twice on one plan,
+    and again after another plan of a different size ran in between, gives the
+    same bits -- no state leaks between launches or plans."""
+    from paper_2312_01121_b200.backends.b200 import B200Backend
+
+    n = {"tiny": 20, "single": 100, "cluster": 100}.get(family, 200)
+    g = np.random.default_rng(31)
+    w = g.uniform(-1, 1, (n, n)) / np.sqrt(n)
+    np.fill_diagonal(w, 0.0)
+    top = sto.Topology(sto.CouplingMatrix(w), sto.InputWeights(g.uniform(-1, 1, (n, 1))))
+    samples = g.uniform(-1, 1, (30, 1))
+    be = B200Backend(top, sto.PhysicalParams(), flags=FORCE[family])
+
+    def once(backend):
+        m = sto.initial_state(n)
+        return backend.integrate_run(m, samples, 2, 1e-11, 60, 10), m
+
+    a, ma = once(be)
+    b, mb = once(be)
+    other = B200Backend(sto.build_topology(77, seed=2), sto.PhysicalParams())
+    once_other = other.integrate_run(sto.initial_state(77), np.zeros((1, 1)), 1, 1e-11, 40, 40)
+    assert np.isfinite(once_other).all()
+    c, mc = once(be)
+    assert_bit_equal(a, b, f"{family}: second run")
+    assert_bit_equal(a, c, f"{family}: after another plan")
+    assert_bit_equal(ma, mc, f"{family}: final state")
