@@ -203,6 +203,11 @@ STO_API int sto_integrate_host(sto_plan *plan, double *m, const double *samples,
 STO_API int sto_tree_matvec(int device, int64_t rows, int64_t cols, const double *a, int64_t lda,
                     const double *x, double *out);
 
+/* out[r] = pinned-tree sum_j W[r][j] * x[j] with the plan's resident W layout
+ * (model.py:176-180 coupling_field_x without the a_cp factor): no W upload per
+ * call.  x (n), out (n): device pointers; asynchronous on `stream`. */
+STO_API int sto_plan_matvec(sto_plan *plan, const double *x, double *out, void *stream);
+
 /* Reservoir construction on the device (topology.py:27-54 RngStream,
  * :241-273 generate_coupling / generate_input_weights, :146-238 spectral_radius
  * matvecs).  pcg = {state_hi, state_lo, inc_hi, inc_lo} of numpy's PCG64(seed)

@@ -109,6 +109,8 @@ SIGNATURES = {
                                      ctypes.c_double, ctypes.c_void_p]),
     "sto_norm_drift": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                       ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "sto_plan_matvec": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p]),
     "sto_selftest_div": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_void_p]),
@@ -315,6 +317,10 @@ class Plan:
                                  ctypes.byref(st) if sync else None, _stream_ptr(self.device))
         check(rc, st)
         return st
+
+    def matvec_dev(self, x, out) -> None:
+        """out = pinned-tree W @ x with the plan's resident W (device tensors)."""
+        check(lib().sto_plan_matvec(self._h, x.data_ptr(), out.data_ptr(), _stream_ptr(self.device)))
 
     def integrate_ensemble_dev(self, m, consts, samples, steps_per_sample: int,
                                sample_member_stride: int, dt: float, steps: int, stride: int,

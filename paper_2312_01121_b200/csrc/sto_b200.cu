@@ -1381,6 +1381,25 @@ int sto_tree_matvec(int device, int64_t rows, int64_t cols, const double *a, int
     return rc;
 }
 
+int sto_plan_matvec(sto_plan *P, const double *x, double *out, void *stream) {
+    if (!P || !x || !out) return fail(STO_E_PARAM, "bad plan matvec arguments");
+    if (P->world > 1) return fail(STO_E_PARAM, "plan matvec needs an unsharded plan");
+    STO_CUDA(cudaSetDevice(P->device));
+    KParams p{};
+    p.cs = P->L.cs;
+    p.rows = P->n;
+    p.mode = kMatvec;
+    p.w = P->L.w;
+    p.xsrc = x;
+    p.x_stride = 1;
+    p.out = out;
+    const int g = std::min(P->sm_count, P->n);
+    p.rows_cap = (P->n + g - 1) / g;
+    p.chunk_cols = choose_chunk(P->L.cs, p.rows_cap, false);
+    const size_t smem = grid_smem(p.rows_cap, P->L.cs, p.chunk_cols, false);
+    return launch_grid<WSrc::GlobalL2, false>(p, g, smem, false, (cudaStream_t)stream);
+}
+
 #ifdef STO_TIMELINE
 STO_API int sto_debug_ens_timeline(unsigned long long *out, int count) {
     STO_CUDA(cudaMemcpyFromSymbol(out, g_ens_timeline, sizeof(unsigned long long) * count));

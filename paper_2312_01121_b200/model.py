@@ -102,10 +102,49 @@ def spin_torque_strength(m, params, consts=None) -> np.ndarray:
     return consts.h_s_prefactor / (1.0 + params.lambda_stt * mdotp)
 
 
+_MATVEC_PLANS: dict = {}  # id(coupling) -> (weakref(coupling), Plan)
+
+
+def _matvec_plan_for(coupling):
+    """One device plan (W layout resident) per CouplingMatrix object, reused by
+    every coupling_field_x call on it; dies with the object."""
+    import weakref
+
+    from . import _native
+
+    key = id(coupling)
+    hit = _MATVEC_PLANS.get(key)
+    if hit is None or hit[0]() is not coupling:
+        import os
+
+        n = coupling.n
+        if hasattr(coupling, "tensor"):  # DeviceCouplingMatrix: W already on its GPU
+            w, device = coupling.tensor, coupling.tensor.device.index
+        else:
+            w, device = coupling.entries, int(os.environ.get("SPINOSC_GPU_DEVICE", 0))
+        plan = _native.Plan(w, np.zeros((n, 1)), [0.0] * 11, device=device)
+        hit = (weakref.ref(coupling, lambda _r, k=key: _MATVEC_PLANS.pop(k, None)), plan)
+        _MATVEC_PLANS[key] = hit
+    return hit[1]
+
+
 def coupling_field_x(coupling, m_x, a_cp: float) -> np.ndarray:
-    """a_cp (W_cp m^x) with the pinned tree on the GPU (ref `model.py:176-180`)."""
-    entries = getattr(coupling, "entries", coupling)
-    return a_cp * tree_matvec(np.asarray(entries, dtype=np.float64), np.asarray(m_x, dtype=np.float64))
+    """a_cp (W_cp m^x) with the pinned tree on the GPU (ref `model.py:176-180`).
+
+    For a CouplingMatrix the device plan (W uploaded and laid out once) is cached
+    on the object, so a call costs the m^x upload and one matvec launch
+    (`sto_plan_matvec`); a raw array goes through the one-shot `tree_matvec`."""
+    m_x = np.asarray(m_x, dtype=np.float64)
+    if hasattr(coupling, "entries") and hasattr(coupling, "n"):
+        import torch
+
+        plan = _matvec_plan_for(coupling)
+        dev = torch.device("cuda", plan.device)
+        x = torch.as_tensor(np.ascontiguousarray(m_x)).to(dev)
+        out = torch.empty(coupling.n, dtype=torch.float64, device=dev)
+        plan.matvec_dev(x, out)
+        return a_cp * out.cpu().numpy()
+    return a_cp * tree_matvec(np.asarray(coupling, dtype=np.float64), m_x)
 
 
 def input_field_x(weights, u, a_in: float) -> np.ndarray:

@@ -173,6 +173,30 @@ def test_total_b_matches_reference(plugged):
 
 
 @pytest.mark.gpu
+def test_coupling_field_plan_cached_and_bit_exact(plugged):
+    """coupling_field_x on a CouplingMatrix reuses one device plan per matrix
+    object (sto_plan_matvec, no W upload per call) and stays bit-identical to
+    the reference's numpy pinned tree (ref model.py:176-180), also for a raw
+    array (the one-shot path)."""
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200 import model
+
+    n = 300
+    top_ref = plugged.build_topology(n, seed=9)
+    cm = sto.CouplingMatrix(top_ref.coupling.entries)
+    g = np.random.default_rng(10)
+    before = len(model._MATVEC_PLANS)
+    for _ in range(3):
+        mx = g.uniform(-1, 1, n)
+        got = sto.coupling_field_x(cm, mx, 0.7)
+        want = plugged.coupling_field_x(top_ref.coupling, mx, 0.7)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+        raw = sto.coupling_field_x(top_ref.coupling.entries, mx, 0.7)
+        assert np.array_equal(raw.view(np.uint64), want.view(np.uint64))
+    assert len(model._MATVEC_PLANS) == before + 1
+
+
+@pytest.mark.gpu
 def test_integration_md_ctypes_stub_runs(plugged):
     """the ctypes stub a spinosc maintainer would paste -- executed
     verbatim (library path substituted) and checked against spinosc's own fused backend."""
