@@ -596,8 +596,19 @@ __global__ void __launch_bounds__(32, 1) tiny_rk4_kernel(const __grid_constant__
     // kG steps per proof check: the branch on the proofs (and, for n > 1, the
     // warp vote) is paid once per group; a failed proof replays the group
     // from its saved start state with the library division.
+    // h_s = pref / d with pref == 0 (zero drive current) is an exact +-0 the
+    // speculative proof rejects (its exponent guard), so such runs skip the
+    // speculation instead of replaying every group
+    const bool use_spec = c.pref != 0.0;
     auto rk4_group = [&](auto group) {
         constexpr int kG = decltype(group)::value;
+        if (!use_spec) {
+            for (int g = 0; g < kG; ++g) {
+                m = rk4_body(std::false_type{}, nullptr);
+                publish(m.x);
+            }
+            return;
+        }
         const V3 m_save = m;
         bool ok = true;
 #pragma unroll
