@@ -426,3 +426,25 @@ def test_numpy_norm_order_pinned():
     want = np.linalg.norm(v, axis=-1)
     got = np.sqrt((v[:, 0] * v[:, 0] + v[:, 1] * v[:, 1]) + v[:, 2] * v[:, 2])
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_integrate_ensemble_argument_checks_before_any_device_work():
+    """integrate_ensemble validates its arguments (ref-style ParameterError)
+    before a backend exists, so they hold on a host without a GPU."""
+    import pytest
+
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200.errors import ParameterError
+
+    top = sto.Topology.decoupled(8)
+    cfg = sto.RunConfig(n=8, steps=10, dt=1e-11)
+    params = [sto.PhysicalParams()] * 3
+    with pytest.raises(ParameterError):
+        sto.integrate_ensemble(top, [], cfg)
+    with pytest.raises(ParameterError):
+        sto.integrate_ensemble(sto.Topology.decoupled(9), params, cfg)
+    with pytest.raises(ParameterError):
+        sto.integrate_ensemble(top, params, cfg, m0=np.zeros((2, 8, 3)))
+    with pytest.raises(ParameterError):
+        sto.integrate_ensemble(top, params, cfg,
+                               input_series=[sto.InputSeries.zeros(1)] * 2)
