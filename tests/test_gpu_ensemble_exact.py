@@ -102,6 +102,39 @@ def test_every_tile_height(sto, oracle_mod, monkeypatch, u):
     _check(sto, oracle_mod, top, _sweep(sto, batch), cfg, (0, 37, 64, 69))
 
 
+def test_many_tiles_per_cta(sto, oracle_mod, monkeypatch):
+    """More tiles than SMs: every CTA walks several tiles per stage (here 8-row
+    tiles, N = 1000, B = 640 -> 1250 tiles, ~9 per CTA), including the per-
+    column counters of tiles that share a CTA."""
+    monkeypatch.setenv("STO_EX_U", "1")
+    n, batch, steps = 1000, 640, 30
+    top = _rand_top(sto, n, seed=41)
+    series = sto.InputSeries(np.random.default_rng(42).uniform(-1, 1, (steps, 1)), 1)
+    cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=10, input_series=series)
+    _check(sto, oracle_mod, top, _sweep(sto, batch), cfg, (0, 63, 64, 333, 639))
+
+
+def test_many_tiles_per_cta_divergence(sto, monkeypatch):
+    """Record-step stop with several tiles per CTA: only the diverging member's
+    column stops early, the others run on; the earliest (step, member) wins."""
+    monkeypatch.setenv("STO_EX_U", "1")
+    n, batch = 64, 2500  # 8 row tiles x 40 member tiles = 320 tiles > 148 CTAs
+    top = sto.Topology(sto.CouplingMatrix.zeros(n), sto.InputWeights(np.ones((n, 1))))
+    params = [sto.PhysicalParams()] * batch
+    series = []
+    for b in range(batch):
+        u = np.zeros((20, 1))
+        if b == 2400:
+            u[3:] = 1e300   # diverges in steps 16..20 -> recording step 20
+        if b == 7:
+            u[7:] = 1e300   # later: steps 36..40 -> recording step 40
+        series.append(sto.InputSeries(u, 5))
+    cfg = sto.RunConfig(n=n, steps=100, dt=1e-11, record_stride=5)
+    with pytest.raises(sto.IntegrationDivergedError) as info:
+        sto.integrate_ensemble(top, params, cfg, input_series=series, exact=True)
+    assert info.value.member == 2400 and info.value.step == 20
+
+
 def test_several_launches(sto, oracle_mod, monkeypatch):
     monkeypatch.setenv("STO_EX_CT_PER_LAUNCH", "1")
     n, batch = 64, 150
@@ -156,13 +189,27 @@ def test_exact_divergence_reports_first_member_and_stops(sto):
 
 
 @settings(max_examples=fuzz_examples(25), deadline=None, suppress_health_check=list(HealthCheck))
-@given(n=st.integers(1, 300), batch=st.integers(1, 140), steps=st.integers(1, 60),
-       stride=st.integers(1, 25), sps=st.integers(1, 7), seed=st.integers(0, 2**31 - 1))
-def test_random_exact_ensembles(sto, oracle_mod, n, batch, steps, stride, sps, seed):
+@given(n=st.integers(1, 300), batch=st.integers(1, 400), steps=st.integers(1, 60),
+       stride=st.integers(1, 25), sps=st.integers(1, 7), u=st.integers(0, 7),
+       seed=st.integers(0, 2**31 - 1))
+def test_random_exact_ensembles(sto, oracle_mod, n, batch, steps, stride, sps, u, seed):
+    """Random sizes, drives, member parameters and tile heights (u = 0: the
+    host's choice; small u with large B gives several tiles per CTA)."""
+    import os
+
     g = np.random.default_rng(seed)
     top = _rand_top(sto, n, seed=seed)
     params = [sto.PhysicalParams(current=float(c), h_appl=float(h))
               for c, h in zip(g.uniform(1e-3, 4e-3, batch), g.uniform(0, 500, batch))]
     series = sto.InputSeries(g.uniform(-1, 1, ((steps + sps - 1) // sps, 1)), sps)
     cfg = sto.RunConfig(n=n, steps=steps, dt=1e-11, record_stride=stride, input_series=series)
-    _check(sto, oracle_mod, top, params, cfg, sorted({0, batch - 1, int(g.integers(batch))}))
+    old = os.environ.get("STO_EX_U")
+    if u:
+        os.environ["STO_EX_U"] = str(u)
+    try:
+        _check(sto, oracle_mod, top, params, cfg, sorted({0, batch - 1, int(g.integers(batch))}))
+    finally:
+        if old is None:
+            os.environ.pop("STO_EX_U", None)
+        else:
+            os.environ["STO_EX_U"] = old
