@@ -185,6 +185,31 @@ def test_ensemble_divergence_earliest_step_across_half_columns(sto):
     assert info.value.member == 130 and info.value.step == 15
 
 
+@pytest.mark.parametrize("exact", [False, True])
+def test_divergence_across_launches(sto, monkeypatch, exact):
+    """Members split over several sequential launches (DMMA: 8 member columns
+    per launch at N = 1000; exact: one member tile per launch): a member of a
+    LATER launch that diverges at an EARLIER step is still the one reported."""
+    if exact:
+        monkeypatch.setenv("STO_EX_CT_PER_LAUNCH", "1")
+    n, batch, sps = 1000, 640, 5
+    w_in = np.ones((n, 1))
+    top = sto.Topology(sto.CouplingMatrix.zeros(n), sto.InputWeights(w_in))
+    params = [sto.PhysicalParams()] * batch
+    series = []
+    for b in range(batch):
+        u = np.zeros((12, 1))
+        if b == 3:
+            u[6:] = 1e300    # launch 1: diverges in steps 31..35 -> recording step 35
+        if b == 600:
+            u[2:] = 1e300    # last launch: steps 11..15 -> recording step 15
+        series.append(sto.InputSeries(u, sps))
+    cfg = sto.RunConfig(n=n, steps=60, dt=1e-11, record_stride=5)
+    with pytest.raises(sto.IntegrationDivergedError) as info:
+        sto.integrate_ensemble(top, params, cfg, input_series=series, exact=exact)
+    assert info.value.member == 600 and info.value.step == 15
+
+
 def _rand_top(sto, n, n_in=1, seed=0):
     g = np.random.default_rng(seed)
     w = g.uniform(-1, 1, (n, n)) / np.sqrt(max(n, 3) / 3.0)
