@@ -44,6 +44,29 @@ def test_logical_ranks_bit_exact(oracle_mod, monkeypatch, n, world, fam, chunk):
     assert_bit_equal(m, want[-1], "final m")
 
 
+@pytest.mark.parametrize("fam", [0, 0x1])
+def test_logical_ranks_multichannel_held_drive(oracle_mod, fam):
+    """Sharded rows with n_in = 3 and a held drive (each rank's W_in shard, the
+    input field's tree over channels, the sample index): bit-exact."""
+    import paper_2312_01121_b200 as sto
+    from paper_2312_01121_b200.sharding import integrate_logical
+
+    n, world, n_in, sps, steps = 1500, 3, 3, 4, 38
+    g = np.random.default_rng(77)
+    w = g.uniform(-1, 1, (n, n)) / np.sqrt(n / 3.0)
+    np.fill_diagonal(w, 0.0)
+    w_in = g.uniform(-1, 1, (n, n_in))
+    top = sto.Topology(sto.CouplingMatrix(w), sto.InputWeights(w_in))
+    samples = g.uniform(-1, 1, ((steps + sps - 1) // sps, n_in))
+    consts = sto.kernel_scalars(sto.PhysicalParams())
+    want, _ = oracle_mod.integrate(w, w_in, consts, sto.initial_state(n), samples, sps, 1e-11,
+                                   steps, 6)
+    m = sto.initial_state(n)
+    got = integrate_logical(top, sto.PhysicalParams(), m, samples, sps, 1e-11, steps, 6, world,
+                            flags=fam)
+    assert_bit_equal(got, want, "n_in=3 held drive, 3 logical ranks")
+
+
 def test_repeated_group_runs_reuse_epochs(oracle_mod):
     """Epochs continue across launches (flags are never reset); two runs in a row."""
     import paper_2312_01121_b200 as sto
