@@ -196,6 +196,27 @@ def test_llg_derivative_consts_and_plan_cache(sto, oracle_mod):
     assert len(model._BACKENDS[id(top)][1]) == before  # same scalars: the cached plan
 
 
+@pytest.mark.parametrize("n,n_in", [(33, 3), (500, 5), (3000, 2)])
+def test_derivative_multichannel_against_oracle(sto, oracle_mod, n, n_in):
+    """K0 (the reference plugin contract, derivative(m, u, out)) with n_in > 1:
+    the input field is the pinned tree over the channels (cpu_jit.py:48-87)."""
+    from paper_2312_01121_b200.backends.b200 import B200Backend
+
+    g = np.random.default_rng(n)
+    w = g.uniform(-1, 1, (n, n)) / np.sqrt(n)
+    np.fill_diagonal(w, 0.0)
+    w_in = g.uniform(-1, 1, (n, n_in))
+    top = sto.Topology(sto.CouplingMatrix(w), sto.InputWeights(w_in))
+    m = g.normal(size=(n, 3))
+    m /= np.linalg.norm(m, axis=1, keepdims=True)
+    u = g.uniform(-1, 1, n_in)
+    be = B200Backend(top, sto.PhysicalParams())
+    out = np.empty((n, 3))
+    be.derivative(m, u, out)
+    want = oracle_mod.derivative(w, w_in, sto.kernel_scalars(sto.PhysicalParams()), m, u)
+    assert_bit_equal(out, want, f"K0 n={n} n_in={n_in}")
+
+
 def test_derivative_on_device_tensors(sto):
     import torch
 
