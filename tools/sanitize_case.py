@@ -50,6 +50,7 @@ CASES = {
     "ensemble_u7": ("ens", 200, 3, 1, {"STO_ENS_U": "7"}),
     "ensemble_exact": ("ensx", 200, 3, 1, {}),
     "ensemble_exact_2launch": ("ensx", 100, 2, 1, {"STO_EX_CT_PER_LAUNCH": "1"}),
+    "ensemble_exact_multitile": ("ensx", 600, 2, 1, {"STO_EX_U": "1"}),
     "derivative_k0": ("deriv", 900, 0, 0, {}),
     "tiny_n1_spec": ("auto", 1, 40, 10, {}),
     "device_build": ("build", 300, 0, 0, {}),
